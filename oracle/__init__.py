@@ -1,0 +1,125 @@
+"""Python face of the C oracle (oracle/bl_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` legs are the only callers.  The product
+package `paper_2002_08233_b200` never imports this module, and this module
+never imports the product package.
+
+Functions mirror the paper's operations (§2.2, Alg. 1
+P:542-569, Alg. 2); see bl_oracle.c for the header and DESIGN.md
+§3 for the readings.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bl_oracle.c")
+_IMPL = os.path.join(_HERE, "bl_oracle_impl.h")
+_SO = os.path.join(_HERE, "libbl_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+REPULSE_NEIGHBORS = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc: -O2 -ffp-contract=off, no fast-math."""
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_IMPL))
+    if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= newest:
+        return _SO
+    tmp = _SO + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+           "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, _SO)
+    return _SO
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        lib = ctypes.CDLL(build())
+        i32, u32, dbl, flt = ctypes.c_int32, ctypes.c_uint32, ctypes.c_double, ctypes.c_float
+        vp = ctypes.c_void_p
+        for sfx, R in (("f64", dbl), ("f32", flt)):
+            f = getattr(lib, f"oracle_layout_{sfx}")
+            f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, dbl, dbl, i32, u32, vp, vp, ctypes.c_int]
+            f.restype = ctypes.c_int
+            f = getattr(lib, f"oracle_forces_{sfx}")
+            f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, u32, vp, ctypes.c_int]
+            f.restype = ctypes.c_int
+            f = getattr(lib, f"oracle_apply_update_{sfx}")
+            f.argtypes = [vp, R, R, R, vp]
+            f.restype = ctypes.c_int
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _csr(rowptr, colidx):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int32)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    if colidx.size == 0:
+        colidx = np.zeros(1, dtype=np.int32)  # valid pointer, never read
+    return rowptr, colidx
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
+           cooling=0.999, max_batches=0, flags=0, threads=0, precision="f64"):
+    """Run Alg. 2 from xy0 ((n,2) any float dtype; converted to the oracle's
+    precision).  Returns (xy (n,2), energy[iters] fp64, iters_done)."""
+    lib = _load()
+    dt = np.float64 if precision == "f64" else np.float32
+    xy = np.ascontiguousarray(np.asarray(xy0, dtype=dt).reshape(n, 2)).copy()
+    rowptr, colidx = _csr(rowptr, colidx)
+    energy = np.zeros(max(iters, 1), dtype=np.float64)
+    done = ctypes.c_int32(0)
+    fn = getattr(lib, f"oracle_layout_{precision}")
+    rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0, cooling,
+            max_batches, flags, _ptr(energy), ctypes.byref(done), threads)
+    if rc != 0:
+        raise ValueError("oracle_layout: invalid arguments")
+    return xy, energy[:iters], int(done.value)
+
+
+def forces(n, rowptr, colidx, xy, first=0, count=None, *, K=1.0, C=1.0, flags=0,
+           threads=0, precision="f64"):
+    """f(i, c) of §2.2 for i in [first, first+count) at state xy; (count, 2)."""
+    lib = _load()
+    if count is None:
+        count = n - first
+    dt = np.float64 if precision == "f64" else np.float32
+    c = np.ascontiguousarray(np.asarray(xy, dtype=dt).reshape(n, 2))
+    rowptr, colidx = _csr(rowptr, colidx)
+    out = np.zeros((max(count, 1), 2), dtype=dt)
+    fn = getattr(lib, f"oracle_forces_{precision}")
+    rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(c), first, count, K, C, flags, _ptr(out), threads)
+    if rc != 0:
+        raise ValueError("oracle_forces: invalid arguments")
+    return out[:count]
+
+
+def apply_update(ci, f, step, precision="f64"):
+    """c_i + step * f/||f|| (Alg. 1 line 12); returns (new c_i, ||f||^2)."""
+    lib = _load()
+    dt = np.float64 if precision == "f64" else np.float32
+    c = np.ascontiguousarray(np.asarray(ci, dtype=dt).reshape(2)).copy()
+    q = np.zeros(1, dtype=dt)
+    getattr(lib, f"oracle_apply_update_{precision}")(_ptr(c), float(f[0]), float(f[1]), float(step), _ptr(q))
+    return c, float(q[0])
