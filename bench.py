@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- BatchLayout exact path on B200 (one JSON line on rank 0).
+
+A "step" is one whole C-ABI layout call over the workload (default C5:
+R-MAT scale 18, n = 262,144, b = 1024, 50 iterations = 12,800 dependent
+batches, exact all-pairs repulsion), i.e. one pass of every §8(a) row.
+Metric (BASELINE.json): pair interactions/s = iters * n(n-1) / T, plus
+iterations/s and the fraction of the FP32/SFU issue roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5]
+  python bench.py --impl reference ...   # the oracle (CPU) as reference arm
+
+Multi-GPU (torchrun): replicas only -- each rank lays out its own copy of
+the workload (independent problems, no data-path collective); value = all
+ranks' pairs / max-over-ranks device time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "pair interactions/sec"
+UNIT = "pair/s"
+MUFU_PER_CLK_SM = 16  # SFU lanes per SM per clock
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (identity at world 1)."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def workload_desc(name, g, cfg):
+    return {
+        "workload": f"{name}: {cfg.desc}, batch {cfg.batch}, {cfg.iters} iterations, exact all-pairs "
+                    "repulsion, fp32 coords U[0,1)^2 seed 42",
+        "n": g.n, "nnz": int(g.nnz), "batch": cfg.batch, "iters": cfg.iters,
+        "K": cfg.K, "C": cfg.C, "step0": cfg.step0, "cooling": cfg.cooling,
+    }
+
+
+# ------------------------------------------------------------------ oracle leg
+def oracle_sample(g, xy0, cfg, seconds: float, threads: int = 0):
+    """Time the oracle (as it stands) on a bounded prefix of the workload:
+    the first k batches of iteration 0, k calibrated to ~`seconds`."""
+    import oracle
+    b = min(cfg.batch, g.n)
+    t0 = time.perf_counter()
+    oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=1, batch=b, max_batches=1, threads=threads)
+    t1 = time.perf_counter() - t0
+    nb = (g.n + b - 1) // b
+    k = int(max(1, min(nb * cfg.iters, seconds / max(t1, 1e-6))))
+    return k, t1
+
+
+def run_oracle(g, xy0, cfg, k, threads=0):
+    import oracle
+    b = min(cfg.batch, g.n)
+    t0 = time.perf_counter()
+    oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=cfg.iters, batch=b, max_batches=k,
+                  threads=threads)
+    dt = time.perf_counter() - t0
+    nb = (g.n + b - 1) // b
+    pairs = 0
+    for t in range(k):
+        lo = (t % nb) * b
+        pairs += min(b, g.n - lo) * (g.n - 1)
+    return pairs, dt
+
+
+def cpu_cores():
+    import oracle
+    return int(oracle.max_threads())
+
+
+# ------------------------------------------------------------------ main arms
+def bench_reference(args, name, g, xy0, cfg, rank, world):
+    if rank != 0:
+        return 0
+    k, t1 = oracle_sample(g, xy0, cfg, args.ref_seconds)
+    for _ in range(args.warmup):
+        run_oracle(g, xy0, cfg, max(1, k // 4))
+    tot_pairs, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        p, dt = run_oracle(g, xy0, cfg, k)
+        tot_pairs += p
+        tot_t += dt
+    value = tot_pairs / tot_t
+    b = min(cfg.batch, g.n)
+    sample = (f"first {k} batch update(s) of iteration 0 of {name} (b={b}, each {b}x{g.n - 1} "
+              f"pairs) per step; oracle fp64, OpenMP over batch vertices")
+    cores = cpu_cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_desc(name, g, cfg),
+        "iters_per_sec": value / (g.n * (g.n - 1.0)),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
+    import torch
+
+    import paper_2002_08233_b200 as bl
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    params = dict(iters=cfg.iters, batch=cfg.batch, K=cfg.K, C=cfg.C, step0=cfg.step0,
+                  cooling=cfg.cooling)
+    lay = bl.BatchLayout(g.n, g.rowptr, g.colidx)
+    d_xy0 = torch.from_numpy(xy0.copy()).to(dev)
+    d_xy = torch.empty_like(d_xy0)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        d_xy.copy_(d_xy0)
+        lay.layout_device(d_xy, stream=stream, **params)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))                 # evict L2 between timed steps
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            launches += bl.bl_last_launch_count(lay.h)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = sum(ms) / 1e3
+    t_max = max_over_ranks(t_local, world, dev if world > 1 and args.backend == "nccl" else None)
+    pairs_per_step = cfg.iters * g.n * (g.n - 1.0)
+    value = world * args.steps * pairs_per_step / t_max
+    e_last, trace, done = lay.energy(trace_len=cfg.iters)
+    assert done == cfg.iters
+
+    # ---- e2e through the host C-ABI call (H2D + kernel + D2H inside bl_layout)
+    e2e_steps = max(1, min(args.steps, 3))
+    h_xy = torch.from_numpy(xy0.copy()).pin_memory().numpy()
+    tot = 0.0
+    for _ in range(e2e_steps):
+        buf = h_xy.copy()
+        flush.fill_(0.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bl.bl_layout(lay.h, buf, bl.bl_params_default(**params))   # includes H2D/D2H of xy
+        e_l, _, _ = lay.energy(trace_len=cfg.iters)                # D2H of the energy trace
+        tot += time.perf_counter() - t0
+    e2e_t = max_over_ranks(tot, world, dev if world > 1 and args.backend == "nccl" else None)
+    e2e_value = world * e2e_steps * pairs_per_step / e2e_t
+
+    peaks, peak_src = load_peaks()
+    clocks = clk.summary()
+    sm_max = float(clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = nsm * MUFU_PER_CLK_SM * sm_max * 1e6
+    achieved = pairs_per_step / (t_local / args.steps)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(workload_desc(name, g, cfg),
+                       l2="flushed (512 MiB write) before every timed step",
+                       parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
+        "iters_per_sec": world * args.steps * cfg.iters / t_max,
+        "roofline": {
+            "bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT,
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "bl_layout_kernel<4> (persistent, cooperative)",
+            "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU.RCP/clk x {sm_max:.0f} MHz "
+                          f"(sm_max_mhz, {peak_src}); 1 MUFU per pair",
+            "frac_at_median_clock": (achieved / (nsm * MUFU_PER_CLK_SM * clocks["sm_mhz"] * 1e6)
+                                     if clocks.get("sm_mhz") else None),
+        },
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * g.n,
+                "d2h_bytes_per_step": 8 * g.n + 8 * cfg.iters},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "energy_final": e_last,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        k, _ = oracle_sample(g, xy0, cfg, args.cpu_seconds)
+        pairs, dt = run_oracle(g, xy0, cfg, k)
+        b = min(cfg.batch, g.n)
+        line["cpu_baseline"] = {
+            "value": pairs / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"first {k} batch update(s) of iteration 0 of {name} (b={b}), {dt:.1f} s",
+        }
+    lay.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+
+    rank, world, local_rank = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(backend=args.backend, init_method="env://")
+
+    from blgen import build_config
+    g, xy0, cfg = build_config(args.config)
+    if args.impl == "reference":
+        rc = bench_reference(args, args.config, g, xy0, cfg, rank, world)
+    else:
+        rc = bench_ours(args, args.config, g, xy0, cfg, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,128 @@
+/*
+ * bl.h -- C-ABI of libbl, the B200 (sm_100a) BatchLayout exact-path library.
+ *
+ * Method: "BatchLayout" (Rahman, Sujon & Azad, arXiv:2002.08233), the exact
+ * minibatch force-directed layout of Alg. 2 with the
+ * spring-electrical (2,-1) force model of §2.2.  Citations
+ * "P:n" are lines of the paper's text; readings of points the
+ * paper leaves open are C1-C13 in DESIGN.md §3.
+ *
+ * All functions are extern "C"; no C++ exception crosses this boundary.
+ * The library links the CUDA runtime only (no torch); callers may hand in
+ * device pointers and a cudaStream_t obtained from any framework.
+ *
+ * Status codes: every call returns a bl_status; on failure
+ * bl_last_error(h) holds a one-line message for calls that took a handle.
+ */
+#ifndef BL_H_
+#define BL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bl_ctx bl_ctx; /* opaque; owns the device CSR and all scratch */
+
+typedef enum {
+  BL_OK = 0,
+  BL_EINVAL = -1, /* invalid argument (CSR, params, pointers, sizes)      */
+  BL_ENOMEM = -2, /* host or device allocation failed                      */
+  BL_ECUDA = -3,  /* a CUDA call or the cooperative launch failed          */
+  BL_ESTATE = -4  /* call order: e.g. bl_energy before any layout          */
+} bl_status;
+
+/* flags */
+enum {
+  /* Reading C2: by default adjacent pairs ATTRACT ONLY, as in the if/else of
+   * Alg. 1 / Alg. 2 and the (i,j) not-in-E second
+   * sum of §2.2.  With this flag adjacent pairs also repel (the
+   * classic Fruchterman-Reingold form, and the BH variant Alg. S3). */
+  BL_REPULSE_NEIGHBORS = 1u << 0
+};
+
+typedef struct {
+  int32_t iters;       /* >= 0; MaxIteration of Alg. 2. 0 = no-op      */
+  int32_t batch;       /* >= 1; BS of Alg. 2. > n is clamped to n  */
+  float K;             /* > 0; optimal spring length of §2.2. Unstated
+                          in the paper (reading C6); default 1                  */
+  float C;             /* >= 0; the paper's R, relative strength;
+                          default 1 (reading C6)                               */
+  float step0;         /* > 0; initial Step, Alg. 2 P:700 (1.0)                */
+  float cooling;       /* (0, 1]; Step *= cooling per iteration, P:730 (0.999) */
+  double tol;          /* >= 0; stop when |E_t - E_{t-1}| < tol (P:1082,
+                          §4.5).  0 disables.                                  */
+  int32_t max_batches; /* > 0: stop after that many batch updates in total
+                          (debug / one-batch parity); <= 0: no limit           */
+  uint32_t flags;      /* BL_REPULSE_NEIGHBORS                                 */
+} bl_params;
+
+/* Fill p with the paper's defaults: iters 600 (the CLI default),
+ * batch 256, K = 1, C = 1, step0 = 1.0, cooling = 0.999, tol = 0,
+ * max_batches = 0, flags = 0. */
+void bl_params_default(bl_params *p);
+
+/* Create a context on the current CUDA device for the undirected graph G
+ * given in CSR: rowptr int32[n+1], colidx int32[rowptr[n]],
+ * host memory, owned by the caller (copied; may be freed on return).
+ * Validation (-> BL_EINVAL): n >= 1, rowptr[0] = 0, rowptr nondecreasing,
+ * rowptr[n] = nnz, colidx in [0, n), no self loops, rows strictly
+ * ascending, symmetric (undirected graphs only).  Also n must fit the
+ * resident-coordinate design (n <= bl_max_vertices()).
+ * *out receives the handle on success, NULL otherwise. */
+bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *colidx, bl_ctx **out);
+
+/* Run the layout on HOST coordinates xy (2n floats x0,y0,x1,y1,..., the
+ * initial layout c of Alg. 2 on entry, the final layout on success; left
+ * untouched on failure).  Synchronous: copies xy host->device, runs, copies
+ * back, and records the energy trace.  *iters_done (nullable) receives the
+ * number of completed iterations. */
+bl_status bl_layout(bl_ctx *h, float *xy, const bl_params *p, int32_t *iters_done);
+
+/* Same on DEVICE coordinates d_xy (float2[n], 8-byte aligned, in/out),
+ * enqueued on cuda_stream (a cudaStream_t; NULL = legacy default stream).
+ * Asynchronous: returns after the launch; the energy trace and iteration
+ * count are complete when the stream is.  One persistent cooperative kernel
+ * walks all iters x ceil(n/batch) dependent batches. */
+bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p, void *cuda_stream);
+
+/* Energy (sum_i ||f_i||^2, §2.2; accumulated per batch at each
+ * batch's own time, reset per iteration, Alg. 2 P:703/P:727 -- reading C8)
+ * of the last layout call on h.  Synchronises h's last stream.
+ * e_last (nullable): energy of the last completed iteration.
+ * trace (nullable): up to trace_len per-iteration fp64 energies.
+ * n_written (nullable): entries written to trace.
+ * iters_done (nullable): completed iterations of the last call.
+ * BL_ESTATE if no layout call has completed an iteration. */
+bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t trace_len,
+                    int32_t *n_written, int32_t *iters_done);
+
+/* Debug / parity: the raw combined forces f(i, c) of §2.2 for
+ * i in [first, first+count) at the device state d_xy (not modified), written
+ * to d_f_out (float2[count], device).  Uses the same device code as the
+ * layout kernel.  Only p->K, p->C and p->flags are read. */
+bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int32_t count, float *d_f_out,
+                    const bl_params *p, void *cuda_stream);
+
+/* Largest n the resident design accepts on the current device. */
+int32_t bl_max_vertices(void);
+
+/* Number of kernel launches the last bl_layout_device / bl_layout /
+ * bl_forces call enqueued (the persistent design launches exactly one). */
+int32_t bl_last_launch_count(const bl_ctx *h);
+
+/* Microbenchmark of the roofline denominators on the current device:
+ * sustained warp-instruction rates per SM per clock of (0) 3-register FFMA,
+ * (1) MUFU.RCP (rcp.approx.ftz.f32), (2) MUFU.RSQ, measured with clock64
+ * inside one kernel on every SM.  rates[3] receives ops/clk/SM.  Blocking. */
+bl_status bl_microbench(double rates[3]);
+
+void bl_destroy(bl_ctx *h);
+const char *bl_status_string(bl_status s);
+const char *bl_last_error(const bl_ctx *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BL_H_ */

@@ -1,0 +1,427 @@
+// bl_api.cu -- host side of libbl: the C-ABI declared in include/bl.h.
+//
+// Context = device copy of the CSR + the attraction item lists +
+// all scratch.  Each layout call is ONE cooperative launch of the persistent
+// kernel in bl_kernel.cuh (the paper forks OpenMP once per batch, P:961-966;
+// here the dependent batches are walked on the device with grid barriers).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bl.h"
+#include "bl_kernel.cuh"
+
+struct bl_ctx {
+  int32_t n = 0, nnz = 0;
+  int device = 0, num_sms = 0;
+  int G = 0;  // grid size of the persistent kernel
+  int T = 4;  // register-blocked targets per thread
+  // device CSR + items
+  int *d_rowptr = nullptr, *d_colidx = nullptr;
+  int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
+  std::vector<int> item_ptr;  // host copy (per-batch maxima)
+  int n_items = 0;
+  // scratch
+  float2 *d_part = nullptr;
+  size_t part_cap = 0;  // float2 elements
+  float2 *d_attr = nullptr;
+  size_t attr_cap = 0;
+  double *d_e_cta = nullptr;
+  double *d_energy = nullptr;
+  size_t energy_cap = 0;
+  int *d_iters_done = nullptr;
+  unsigned *d_bar = nullptr;
+  float2 *d_xy_host_path = nullptr;  // staging for bl_layout (host xy)
+  size_t xy_cap = 0;
+  // state of the last call
+  cudaStream_t last_stream = nullptr;
+  int32_t last_iters = 0;
+  bool have_layout = false;
+  int32_t launches = 0;
+  std::string err;
+};
+
+static thread_local std::string g_create_err;
+
+static bl_status fail(bl_ctx *h, bl_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h)
+    h->err = buf;
+  else
+    g_create_err = buf;
+  return s;
+}
+
+#define BL_CUDA(h, call)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail((h), e_ == cudaErrorMemoryAllocation ? BL_ENOMEM : BL_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+extern "C" void bl_params_default(bl_params *p) {
+  if (!p) return;
+  p->iters = 600;
+  p->batch = 256;
+  p->K = 1.0f;
+  p->C = 1.0f;
+  p->step0 = 1.0f;
+  p->cooling = 0.999f;
+  p->tol = 0.0;
+  p->max_batches = 0;
+  p->flags = 0;
+}
+
+extern "C" const char *bl_status_string(bl_status s) {
+  switch (s) {
+    case BL_OK: return "BL_OK";
+    case BL_EINVAL: return "BL_EINVAL: invalid argument";
+    case BL_ENOMEM: return "BL_ENOMEM: out of memory";
+    case BL_ECUDA: return "BL_ECUDA: CUDA error";
+    case BL_ESTATE: return "BL_ESTATE: invalid call order";
+  }
+  return "unknown bl_status";
+}
+
+extern "C" const char *bl_last_error(const bl_ctx *h) {
+  return h ? h->err.c_str() : g_create_err.c_str();
+}
+
+extern "C" int32_t bl_last_launch_count(const bl_ctx *h) { return h ? h->launches : 0; }
+
+static size_t smem_bytes(int chunk4, int T) {
+  return (size_t)chunk4 * sizeof(float4) + (size_t)BL_NW * 32 * T * sizeof(float2);
+}
+
+static int chunk4_for(int n, int G) {
+  const int per = (n + G - 1) / G;  // owned sources per CTA (max)
+  return std::max(1, (per + 1) / 2);
+}
+
+static int env_int(const char *name, int def) {
+  const char *s = getenv(name);
+  return (s && *s) ? atoi(s) : def;
+}
+
+template <int T>
+static cudaError_t set_smem_attr(size_t bytes) {
+  return cudaFuncSetAttribute(bl_layout_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)bytes);
+}
+
+extern "C" int32_t bl_max_vertices(void) {
+  int dev = 0, sms = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return 0;
+  const long long room = (long long)optin - 2048 - (long long)BL_NW * 32 * 8 * sizeof(float2);
+  const long long per = room / (long long)sizeof(float4) * 2;
+  const long long n = per * sms;
+  return (int32_t)std::min<long long>(n, 0x7fffffff);
+}
+
+extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *colidx,
+                               bl_ctx **out) {
+  if (!out) return fail(nullptr, BL_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1) return fail(nullptr, BL_EINVAL, "n must be >= 1 (got %d)", n);
+  if (!rowptr) return fail(nullptr, BL_EINVAL, "rowptr is NULL");
+  if (rowptr[0] != 0) return fail(nullptr, BL_EINVAL, "rowptr[0] != 0");
+  for (int32_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] < rowptr[i]) return fail(nullptr, BL_EINVAL, "rowptr decreases at %d", i);
+  const int32_t nnz = rowptr[n];
+  if (nnz > 0 && !colidx) return fail(nullptr, BL_EINVAL, "colidx is NULL");
+  for (int32_t i = 0; i < n; ++i) {
+    for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      const int32_t j = colidx[k];
+      if (j < 0 || j >= n) return fail(nullptr, BL_EINVAL, "colidx[%d]=%d out of range", k, j);
+      if (j == i) return fail(nullptr, BL_EINVAL, "self loop at vertex %d", i);
+      if (k > rowptr[i] && colidx[k - 1] >= j)
+        return fail(nullptr, BL_EINVAL, "row %d not strictly ascending", i);
+    }
+  }
+  // symmetry: every (i, j) has (j, i) -- binary search in row j
+  for (int32_t i = 0; i < n; ++i) {
+    for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      const int32_t j = colidx[k];
+      if (!std::binary_search(colidx + rowptr[j], colidx + rowptr[j + 1], i))
+        return fail(nullptr, BL_EINVAL, "not symmetric: (%d,%d) without (%d,%d)", i, j, j, i);
+    }
+  }
+  const int32_t nmax = bl_max_vertices();
+  if (nmax <= 0) return fail(nullptr, BL_ECUDA, "no usable CUDA device");
+  if (n > nmax)
+    return fail(nullptr, BL_EINVAL, "n=%d exceeds the resident design limit %d", n, nmax);
+
+  bl_ctx *h = new (std::nothrow) bl_ctx();
+  if (!h) return fail(nullptr, BL_ENOMEM, "host allocation failed");
+  h->n = n;
+  h->nnz = nnz;
+  auto bad = [&](bl_status s) {
+    g_create_err = h->err;
+    bl_destroy(h);
+    return s;
+  };
+  if (cudaGetDevice(&h->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess)
+    return bad(fail(h, BL_ECUDA, "no CUDA device"));
+  h->T = env_int("BL_T", 4);
+  if (h->T != 4 && h->T != 8 && h->T != 2) h->T = 4;
+
+  // attraction items: ceil(deg(v)/ECH) per vertex, in vertex order
+  h->item_ptr.assign((size_t)n + 1, 0);
+  for (int32_t v = 0; v < n; ++v) {
+    const int deg = rowptr[v + 1] - rowptr[v];
+    h->item_ptr[v + 1] = h->item_ptr[v] + (deg + BL_ECH - 1) / BL_ECH;
+  }
+  h->n_items = h->item_ptr[n];
+  std::vector<int> item_v(std::max(1, h->n_items)), item_k0(std::max(1, h->n_items));
+  for (int32_t v = 0; v < n; ++v)
+    for (int a = h->item_ptr[v]; a < h->item_ptr[v + 1]; ++a) {
+      item_v[a] = v;
+      item_k0[a] = rowptr[v] + (a - h->item_ptr[v]) * BL_ECH;
+    }
+
+#define ALLOC(ptr, bytes)                                                  \
+  do {                                                                     \
+    cudaError_t e_ = cudaMalloc((void **)&(ptr), (bytes));                 \
+    if (e_ != cudaSuccess) return bad(fail(h, BL_ENOMEM, "cudaMalloc %s: %s", #ptr, cudaGetErrorString(e_))); \
+  } while (0)
+  ALLOC(h->d_rowptr, sizeof(int) * ((size_t)n + 1));
+  ALLOC(h->d_colidx, sizeof(int) * std::max<size_t>(1, nnz));
+  ALLOC(h->d_item_ptr, sizeof(int) * ((size_t)n + 1));
+  ALLOC(h->d_item_v, sizeof(int) * item_v.size());
+  ALLOC(h->d_item_k0, sizeof(int) * item_k0.size());
+  ALLOC(h->d_iters_done, sizeof(int));
+  ALLOC(h->d_bar, sizeof(unsigned));
+#undef ALLOC
+  auto cp = [&](void *dst, const void *src, size_t bytes) {
+    return cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  if (cp(h->d_rowptr, rowptr, sizeof(int) * ((size_t)n + 1)) != cudaSuccess ||
+      (nnz > 0 && cp(h->d_colidx, colidx, sizeof(int) * (size_t)nnz) != cudaSuccess) ||
+      cp(h->d_item_ptr, h->item_ptr.data(), sizeof(int) * ((size_t)n + 1)) != cudaSuccess ||
+      cp(h->d_item_v, item_v.data(), sizeof(int) * item_v.size()) != cudaSuccess ||
+      cp(h->d_item_k0, item_k0.data(), sizeof(int) * item_k0.size()) != cudaSuccess)
+    return bad(fail(h, BL_ECUDA, "CSR upload failed"));
+
+  // grid: one CTA per SM (BL_CTAS_PER_SM overrides), capped by occupancy
+  const int per_sm = std::max(1, env_int("BL_CTAS_PER_SM", 1));
+  h->G = h->num_sms * per_sm;
+  *out = h;
+  return BL_OK;
+}
+
+extern "C" void bl_destroy(bl_ctx *h) {
+  if (!h) return;
+  cudaFree(h->d_rowptr);
+  cudaFree(h->d_colidx);
+  cudaFree(h->d_item_ptr);
+  cudaFree(h->d_item_v);
+  cudaFree(h->d_item_k0);
+  cudaFree(h->d_part);
+  cudaFree(h->d_attr);
+  cudaFree(h->d_e_cta);
+  cudaFree(h->d_energy);
+  cudaFree(h->d_iters_done);
+  cudaFree(h->d_bar);
+  cudaFree(h->d_xy_host_path);
+  delete h;
+}
+
+static bl_status check_params(bl_ctx *h, const bl_params *p) {
+  if (!p) return fail(h, BL_EINVAL, "params is NULL");
+  if (p->iters < 0) return fail(h, BL_EINVAL, "iters < 0");
+  if (p->batch < 1) return fail(h, BL_EINVAL, "batch < 1");
+  if (!(p->K > 0.f) || !std::isfinite(p->K)) return fail(h, BL_EINVAL, "K must be > 0");
+  if (!(p->C >= 0.f) || !std::isfinite(p->C)) return fail(h, BL_EINVAL, "C must be >= 0");
+  if (!(p->step0 > 0.f) || !std::isfinite(p->step0)) return fail(h, BL_EINVAL, "step0 must be > 0");
+  if (!(p->cooling > 0.f && p->cooling <= 1.f)) return fail(h, BL_EINVAL, "cooling must be in (0,1]");
+  if (!(p->tol >= 0.0) || !std::isfinite(p->tol)) return fail(h, BL_EINVAL, "tol must be >= 0");
+  if (p->flags & ~(uint32_t)BL_REPULSE_NEIGHBORS) return fail(h, BL_EINVAL, "unknown flags");
+  return BL_OK;
+}
+
+template <typename P>
+static bl_status grow(bl_ctx *h, P *&ptr, size_t &cap, size_t need) {
+  if (need <= cap) return BL_OK;
+  cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc((void **)&ptr, need * sizeof(P));
+  if (e != cudaSuccess) return fail(h, BL_ENOMEM, "cudaMalloc scratch: %s", cudaGetErrorString(e));
+  cap = need;
+  return BL_OK;
+}
+
+static int max_items_per_batch(const bl_ctx *h, int b, int first, int count) {
+  int mx = 1;
+  for (int lo = first; lo < first + count; lo += b) {
+    const int hi = std::min(lo + b, first + count);
+    mx = std::max(mx, h->item_ptr[hi] - h->item_ptr[lo]);
+  }
+  return mx;
+}
+
+// Launch the persistent kernel.  forces_mode: one "batch" [first, first+count)
+// whose forces are written to f_out instead of being applied.
+static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
+                        int forces_mode, int first, int count, float2 *f_out) {
+  const int n = h->n;
+  const int b = forces_mode ? std::max(1, count) : std::min(p->batch, n);
+  const int G = h->G;
+  bl_status s;
+  if ((s = grow(h, h->d_part, h->part_cap, (size_t)b * G)) != BL_OK) return s;
+  const int mi = forces_mode ? max_items_per_batch(h, b, first, count)
+                             : max_items_per_batch(h, b, 0, n);
+  if ((s = grow(h, h->d_attr, h->attr_cap, (size_t)mi)) != BL_OK) return s;
+  if (!h->d_e_cta) {
+    size_t cap = 0;
+    if ((s = grow(h, h->d_e_cta, cap, (size_t)2 * G)) != BL_OK) return s;
+  }
+  if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
+
+  BLKParams k{};
+  k.n = n;
+  k.b = b;
+  k.nb = (n + b - 1) / b;
+  k.iters = p->iters;
+  k.max_batches = p->max_batches;
+  k.flags = p->flags;
+  k.ck2 = p->C * p->K * p->K;
+  k.invK = 1.0f / p->K;
+  k.step0 = (double)p->step0;
+  k.cooling = (double)p->cooling;
+  k.tol = p->tol;
+  k.chunk4 = chunk4_for(n, G);
+  k.forces_mode = forces_mode;
+  k.first = first;
+  k.count = count;
+  k.xy = d_xy;
+  k.rowptr = h->d_rowptr;
+  k.colidx = h->d_colidx;
+  k.item_ptr = h->d_item_ptr;
+  k.item_v = h->d_item_v;
+  k.item_k0 = h->d_item_k0;
+  k.part = h->d_part;
+  k.attr = h->d_attr;
+  k.e_cta = h->d_e_cta;
+  k.energy = h->d_energy;
+  k.iters_done = h->d_iters_done;
+  k.bar = h->d_bar;
+  k.f_out = f_out;
+
+  const size_t smem = smem_bytes(k.chunk4, h->T);
+  void *kfn = nullptr;
+  cudaError_t e;
+  switch (h->T) {
+    case 2: e = set_smem_attr<2>(smem); kfn = (void *)bl_layout_kernel<2>; break;
+    case 8: e = set_smem_attr<8>(smem); kfn = (void *)bl_layout_kernel<8>; break;
+    default: e = set_smem_attr<4>(smem); kfn = (void *)bl_layout_kernel<4>; break;
+  }
+  if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
+  int occ = 0;
+  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, BL_NT, smem));
+  if (occ * h->num_sms < G)
+    return fail(h, BL_ECUDA, "cooperative grid %d exceeds residency %d x %d SMs", G, occ, h->num_sms);
+
+  BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+  void *args[] = {&k};
+  BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(BL_NT), args, smem, st));
+  h->launches = 1;
+  return BL_OK;
+}
+
+extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p, void *cuda_stream) {
+  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  h->launches = 0;
+  bl_status s = check_params(h, p);
+  if (s != BL_OK) return s;
+  if (!d_xy) return fail(h, BL_EINVAL, "d_xy is NULL");
+  if (((uintptr_t)d_xy) & 7) return fail(h, BL_EINVAL, "d_xy must be 8-byte aligned");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  h->last_stream = st;
+  h->last_iters = p->iters;
+  if (p->iters == 0) {
+    h->have_layout = false;
+    return BL_OK;
+  }
+  s = launch(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr);
+  if (s != BL_OK) return s;
+  h->have_layout = true;
+  return BL_OK;
+}
+
+extern "C" bl_status bl_layout(bl_ctx *h, float *xy, const bl_params *p, int32_t *iters_done) {
+  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  bl_status s = check_params(h, p);
+  if (s != BL_OK) return s;
+  if (!xy) return fail(h, BL_EINVAL, "xy is NULL");
+  for (int32_t i = 0; i < 2 * h->n; ++i)
+    if (!std::isfinite(xy[i])) return fail(h, BL_EINVAL, "non-finite coordinate at %d", i);
+  if ((s = grow(h, h->d_xy_host_path, h->xy_cap, (size_t)h->n)) != BL_OK) return s;
+  cudaStream_t st = nullptr;
+  BL_CUDA(h, cudaMemcpyAsync(h->d_xy_host_path, xy, sizeof(float2) * h->n, cudaMemcpyHostToDevice, st));
+  s = bl_layout_device(h, reinterpret_cast<float *>(h->d_xy_host_path), p, st);
+  if (s != BL_OK) return s;
+  BL_CUDA(h, cudaMemcpyAsync(xy, h->d_xy_host_path, sizeof(float2) * h->n, cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaStreamSynchronize(st));
+  BL_CUDA(h, cudaGetLastError());
+  if (iters_done) {
+    int d = 0;
+    if (p->iters > 0) BL_CUDA(h, cudaMemcpy(&d, h->d_iters_done, sizeof(int), cudaMemcpyDeviceToHost));
+    *iters_done = d;
+  }
+  return BL_OK;
+}
+
+extern "C" bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t trace_len,
+                               int32_t *n_written, int32_t *iters_done) {
+  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  if (trace_len < 0) return fail(h, BL_EINVAL, "trace_len < 0");
+  if (!h->have_layout) return fail(h, BL_ESTATE, "no layout call has run an iteration");
+  BL_CUDA(h, cudaStreamSynchronize(h->last_stream));
+  int d = 0;
+  BL_CUDA(h, cudaMemcpy(&d, h->d_iters_done, sizeof(int), cudaMemcpyDeviceToHost));
+  if (iters_done) *iters_done = d;
+  const int avail = std::min(d, h->last_iters);
+  if (n_written) *n_written = 0;
+  if (trace && trace_len > 0 && avail > 0) {
+    const int m = std::min(avail, trace_len);
+    BL_CUDA(h, cudaMemcpy(trace, h->d_energy, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    if (n_written) *n_written = m;
+  }
+  if (e_last) {
+    if (avail == 0) return fail(h, BL_ESTATE, "no completed iteration");
+    BL_CUDA(h, cudaMemcpy(e_last, h->d_energy + (avail - 1), sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  return BL_OK;
+}
+
+extern "C" bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int32_t count,
+                               float *d_f_out, const bl_params *p, void *cuda_stream) {
+  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  h->launches = 0;
+  bl_status s = check_params(h, p);
+  if (s != BL_OK) return s;
+  if (!d_xy || !d_f_out) return fail(h, BL_EINVAL, "NULL pointer");
+  if (first < 0 || count < 0 || first > h->n - count)
+    return fail(h, BL_EINVAL, "range [%d, %d+%d) outside [0, %d)", first, first, count, h->n);
+  if (count == 0) return BL_OK;
+  return launch(h, const_cast<float2 *>(reinterpret_cast<const float2 *>(d_xy)), p,
+                (cudaStream_t)cuda_stream, 1, first, count, reinterpret_cast<float2 *>(d_f_out));
+}

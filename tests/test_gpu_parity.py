@@ -1,0 +1,300 @@
+"""GPU (CUDA, through the C-ABI) vs oracle parity.  Marked gpu.
+
+Protocol:
+  * one batch (max_batches=1) and one full iteration from the same seeded
+    state: max |xy_gpu - xy_oracle| <= 1e-4 x extent, at every config;
+  * C5 one-iteration at full size on SAMPLED batches (shadowing: the oracle
+    recomputes batch t from the GPU's own state after batches < t);
+  * per-vertex forces through bl_forces vs the oracle's f(i, c);
+  * determinism (bitwise) and the edge cases of the method.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from blgen import (build_config, cycle_graph, edges_to_csr, grid_graph, rmat_graph, star_graph,
+                   uniform_coords)
+from tests.gpu_helpers import assert_positions_close, extent, gpu_forces, gpu_layout
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["C1", "C2", "C3b64", "C3b256", "C3b1024", "C4", "C5"]
+
+
+def _params(cfg, **kw):
+    d = dict(iters=cfg.iters, batch=cfg.batch, K=cfg.K, C=cfg.C, step0=cfg.step0,
+             cooling=cfg.cooling)
+    d.update(kw)
+    return d
+
+
+def _oracle(g, xy0, p, **kw):
+    q = dict(p)
+    q.update(kw)
+    return oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=q["iters"], batch=q["batch"],
+                         K=q.get("K", 1.0), C=q.get("C", 1.0), step0=q.get("step0", 1.0),
+                         cooling=q.get("cooling", 0.999), max_batches=q.get("max_batches", 0),
+                         flags=q.get("flags", 0))
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_one_batch_parity(name):
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=1, max_batches=1)
+    got, _, _ = gpu_layout(g, xy0, **p)
+    ref, _, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, what=f"{name} one batch")
+    # vertices outside the batch are untouched, bitwise
+    b = min(cfg.batch, g.n)
+    assert np.array_equal(got[b:], xy0[b:])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3b64", "C3b256", "C3b1024", "C4"])
+def test_one_iteration_parity(name):
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=1)
+    got, tr, done = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert done == 1
+    assert_positions_close(got, ref, what=f"{name} one iteration")
+    assert abs(tr[0] - E[0]) <= 1e-3 * E[0], (tr[0], E[0])
+
+
+def test_C5_one_iteration_sampled_batches():
+    """Full-size C5 (n = 262,144, b = 1024): the GPU's state after t batches
+    is loaded into the oracle, which recomputes batch t (forces against all n
+    sources + update) -- compared with the GPU's state after t+1 batches."""
+    g, xy0, cfg = build_config("C5")
+    b = cfg.batch
+    for t in (0, 1, 97, 255):
+        p = _params(cfg, iters=1, max_batches=t)
+        s_t = xy0 if t == 0 else gpu_layout(g, xy0, **p)[0]
+        s_t1, _, _ = gpu_layout(g, xy0, **_params(cfg, iters=1, max_batches=t + 1))
+        lo, hi = t * b, min((t + 1) * b, g.n)
+        assert np.array_equal(s_t1[:lo], s_t[:lo]) and np.array_equal(s_t1[hi:], s_t[hi:])
+        f = oracle.forces(g.n, g.rowptr, g.colidx, s_t, lo, hi - lo)
+        ref = s_t[lo:hi].astype(np.float64) + f / np.hypot(f[:, 0], f[:, 1])[:, None]
+        full_ref = s_t.astype(np.float64).copy()
+        full_ref[lo:hi] = ref
+        ext = extent(full_ref)
+        err = np.abs(s_t1[lo:hi] - ref).max()
+        assert err <= 1e-4 * ext, (t, err, ext)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+def test_forces_parity(name):
+    """bl_forces (same device code) vs oracle f(i, c) for one batch of
+    targets.  Bound: 1e-4 x the sum of term magnitudes sum_j |term_ij| (fp32
+    accumulation of ~n/G-term chunks) + 1e-5 |f_i|."""
+    g, xy0, cfg = build_config(name)
+    first = min(g.n - 1, 3 * cfg.batch) if name != "C5" else 0
+    count = min(cfg.batch, g.n - first)
+    got = gpu_forces(g, xy0, first, count)
+    ref = oracle.forces(g.n, g.rowptr, g.colidx, xy0, first, count)
+    x = xy0.astype(np.float64)
+    bound = np.empty(count)
+    deg = np.diff(g.rowptr)
+    for t in range(count):
+        i = first + t
+        d = np.hypot(x[:, 0] - x[i, 0], x[:, 1] - x[i, 1])
+        d[i] = np.inf
+        nb = g.colidx[g.rowptr[i]:g.rowptr[i + 1]]
+        s = np.sum(1.0 / d) + np.sum(d[nb] ** 2) + 2 * np.sum(1.0 / d[nb])
+        bound[t] = 1e-4 * s + 1e-5 * np.hypot(*ref[t])
+    err = np.hypot(*(got - ref).T)
+    bad = np.nonzero(err > bound)[0]
+    assert bad.size == 0, (bad[:5], err[bad[:5]], bound[bad[:5]], deg[first + bad[:5]])
+
+
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_determinism_bitwise(name):
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=3)
+    a, ea, _ = gpu_layout(g, xy0, **p)
+    b, eb, _ = gpu_layout(g, xy0, **p)
+    assert np.array_equal(a, b) and np.array_equal(ea, eb)
+
+
+def test_host_and_device_paths_agree_bitwise():
+    g, xy0, cfg = build_config("C2")
+    p = _params(cfg, iters=2)
+    a, ea, _ = gpu_layout(g, xy0, device_path=True, **p)
+    b, eb, _ = gpu_layout(g, xy0, device_path=False, **p)
+    assert np.array_equal(a, b) and np.array_equal(ea, eb)
+
+
+# ------------------------------------------------------------ edge cases
+
+def _small(n_rows=10, n_cols=13):
+    g = grid_graph(n_rows, n_cols)
+    return g, uniform_coords(g.n, 5)
+
+
+@pytest.mark.parametrize("b", [1, 7, 64, 129, 130, 1000])
+def test_batch_sizes_including_ragged_and_b_ge_n(b):
+    g, xy0 = _small()
+    p = dict(iters=3, batch=b)
+    got, tr, _ = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, what=f"b={b}")
+    np.testing.assert_allclose(tr, E, rtol=1e-3)
+
+
+def test_single_vertex():
+    g = edges_to_csr(1, np.array([], np.int64), np.array([], np.int64))
+    xy0 = np.array([[0.25, 0.75]], np.float32)
+    got, tr, done = gpu_layout(g, xy0, iters=3, batch=4)
+    assert np.array_equal(got, xy0) and done == 3 and np.all(tr == 0)
+
+
+def test_isolated_vertices_and_hubs():
+    """R-MAT with isolated vertices and rows longer than one attraction item."""
+    g = rmat_graph(12, 16, 0.57, 0.19, 0.19, seed=3)
+    assert np.diff(g.rowptr).max() > 256
+    xy0 = uniform_coords(g.n, 9)
+    p = dict(iters=1, batch=300)
+    got, _, _ = gpu_layout(g, xy0, **p)
+    ref, _, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, what="rmat12")
+
+
+def test_repulse_neighbors_flag():
+    g, xy0 = _small()
+    p = dict(iters=2, batch=32, flags=1)
+    got, _, _ = gpu_layout(g, xy0, **p)
+    ref, _, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, what="flags=1")
+
+
+def test_non_default_K_C_step_cooling():
+    g, xy0 = _small()
+    p = dict(iters=3, batch=50, K=1.7, C=0.3, step0=0.25, cooling=0.9)
+    got, tr, _ = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, what="K,C,step")
+    np.testing.assert_allclose(tr, E, rtol=1e-3)
+
+
+def test_max_batches_mid_iteration():
+    g, xy0 = _small()
+    p = dict(iters=3, batch=40, max_batches=5)   # 4 batches per iteration
+    got, _, done = gpu_layout(g, xy0, **p)
+    ref, _, rdone = _oracle(g, xy0, p)
+    assert done == rdone == 1
+    assert_positions_close(got, ref, what="max_batches")
+
+
+def test_cycle_closed_form_on_gpu():
+    """The oracle's closed-form pin, reached by the GPU too (b = n and b = 1)."""
+    n = 6
+    g = cycle_graph(n)
+    th = 2 * np.pi * np.arange(n) / n + 0.03 * np.sin(np.arange(n))
+    xy0 = np.stack([np.cos(th), np.sin(th)], 1).astype(np.float32)
+    ell = ((n - 3) / 2) ** (1 / 3)
+    for b in (1, n):
+        got, _, _ = gpu_layout(g, xy0, iters=1500, batch=b, cooling=0.99)
+        edge = np.hypot(*(got - np.roll(got, -1, 0)).T)
+        np.testing.assert_allclose(edge, ell, rtol=1e-4)
+
+
+def test_star_closed_form_on_gpu():
+    k = 5
+    g = star_graph(k)
+    th = 2 * np.pi * np.arange(k) / k
+    xy0 = np.vstack([[0, 0], 0.7 * np.stack([np.cos(th), np.sin(th)], 1)]).astype(np.float32)
+    got, _, _ = gpu_layout(g, xy0, iters=1500, batch=1, cooling=0.99)
+    r = np.hypot(*(got[1:] - got[0]).T)
+    np.testing.assert_allclose(r, ((k - 1) / 2) ** (1 / 3), rtol=1e-4)
+
+
+def test_forces_sum_to_zero_b_eq_n():
+    g, xy0 = _small()
+    f = gpu_forces(g, xy0, 0, g.n)
+    assert np.abs(f.sum(0)).max() < 1e-5 * np.abs(f).sum()
+
+
+def test_tol_convergence_stop():
+    """|E_t - E_{t-1}| < tol stops the run; the GPU stops at the same
+    iteration as a stop rule applied to its own trace."""
+    g = cycle_graph(8)
+    th = 2 * np.pi * np.arange(8) / 8
+    xy0 = np.stack([np.cos(th), 1.1 * np.sin(th)], 1).astype(np.float32)
+    _, full, _ = gpu_layout(g, xy0, iters=400, batch=8, cooling=0.98)
+    tol = 1e-3
+    stop = next(t for t in range(1, 400) if abs(full[t] - full[t - 1]) < tol) + 1
+    _, tr, done = gpu_layout(g, xy0, iters=400, batch=8, cooling=0.98, tol=tol)
+    assert done == stop and np.array_equal(tr, full[:stop])
+
+
+def test_iters_zero_is_noop():
+    g, xy0 = _small()
+    got, _, _ = gpu_layout(g, xy0, iters=0, batch=16)
+    assert np.array_equal(got, xy0)
+
+
+def test_full_run_energy_C1_protocol():
+    """Full-run energy (north star: within 1% relative).  The dynamics are
+    chaotic: we require the GPU's final energy to lie within
+    the spread of 5 oracle runs from 1-ulp-perturbed inputs, widened by 1%,
+    and check the first iterations (before chaos) within 1e-3."""
+    g, xy0, cfg = build_config("C1")
+    p = _params(cfg)
+    _, tr, done = gpu_layout(g, xy0, **p)
+    assert done == cfg.iters
+    _, E, _ = _oracle(g, xy0, p)
+    np.testing.assert_allclose(tr[:2], E[:2], rtol=1e-3)
+    finals = [E[-1]]
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        pert = np.nextafter(xy0, np.where(rng.random(xy0.shape) < 0.5, -np.inf, np.inf)
+                            ).astype(np.float32)
+        finals.append(_oracle(g, pert, p)[1][-1])
+    lo, hi = min(finals) * 0.99, max(finals) * 1.01
+    assert lo <= tr[-1] <= hi, (tr[-1], finals)
+
+
+@pytest.mark.parametrize("ckpt", [0, 1, 10, 50, 99])
+def test_shadowing_C1(ckpt):
+    """Shadowing check (v): load the oracle's state x_t into the GPU, run one
+    iteration with step0 = step_t, compare positions and energy."""
+    g, xy0, cfg = build_config("C1")
+    p = _params(cfg)
+    xt, _, _ = _oracle(g, xy0, p, iters=ckpt) if ckpt else (xy0.astype(np.float64), None, None)
+    step_t = 1.0
+    for _ in range(ckpt):
+        step_t *= cfg.cooling
+    xt32 = xt.astype(np.float32)
+    got, tr, _ = gpu_layout(g, xt32, iters=1, batch=cfg.batch, step0=step_t)
+    ref, E, _ = _oracle(g, xt32, dict(iters=1, batch=cfg.batch, step0=step_t))
+    assert_positions_close(got, ref, what=f"shadow t={ckpt}")
+    assert abs(tr[0] - E[0]) <= 1e-4 * E[0]
+
+
+def test_invalid_params_rejected():
+    import paper_2002_08233_b200 as bl
+    g, xy0 = _small()
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        for bad in (dict(batch=0), dict(K=0.0), dict(C=-1.0), dict(step0=0.0), dict(cooling=1.5),
+                    dict(iters=-1), dict(tol=-1.0), dict(flags=8)):
+            with pytest.raises(bl.BLError) as ei:
+                lay.layout(xy0, **bad)
+            assert ei.value.status == bl.BL_EINVAL
+        with pytest.raises(bl.BLError) as ei:
+            lay.energy(1)
+        assert ei.value.status == bl.BL_ESTATE
+        bad_xy = xy0.copy()
+        bad_xy[3, 1] = np.nan
+        with pytest.raises(bl.BLError):
+            lay.layout(bad_xy, iters=1)
+
+
+def test_exactly_one_kernel_launch_per_call():
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0 = _small()
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=5, batch=16)
+        torch.cuda.synchronize()
+        assert bl.bl_last_launch_count(lay.h) == 1
