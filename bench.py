@@ -295,9 +295,35 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
             "sample": f"first {k} batch update(s) of iteration 0 of {name} (b={b}), {dt:.1f} s",
         }
     lay.close()
+    if args.prof and rank == 0:
+        line["phase_profile"] = phase_profile(g, xy0, params, dev, clocks.get("sm_mhz") or sm_max)
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def phase_profile(g, xy0, params, dev, mhz):
+    """One extra (untimed) run with BL_PROFILE=1: CTA-0 phase breakdown (us)
+    and the spread of per-CTA phase-R busy time."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    os.environ["BL_PROFILE"] = "1"
+    try:
+        lay = bl.BatchLayout(g.n, g.rowptr, g.colidx)
+    finally:
+        os.environ.pop("BL_PROFILE", None)
+    d = torch.from_numpy(xy0.copy()).to(dev)
+    lay.layout_device(d, **params)
+    torch.cuda.synchronize()
+    pr = bl.bl_debug_profile(lay.h).astype(np.float64) / mhz  # cycles -> us
+    lay.close()
+    names = ["attraction", "repulsion_sweep", "cta_combine", "barrier1_wait", "update",
+             "barrier2_wait", "tail", "unused"]
+    busy = pr[8:]
+    return {"cta0_us": {k: round(float(v), 1) for k, v in zip(names, pr[:8])},
+            "phaseR_busy_us": {"min": float(busy.min()), "median": float(np.median(busy)),
+                               "max": float(busy.max())}}
 
 
 def main(argv=None):
@@ -311,6 +337,7 @@ def main(argv=None):
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", default="nccl")
+    ap.add_argument("--prof", action="store_true", help="add a phase profile (extra untimed run)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -49,8 +49,10 @@ typedef struct {
                           in the paper (reading C6); default 1                  */
   float C;             /* >= 0; the paper's R, relative strength;
                           default 1 (reading C6)                               */
-  float step0;         /* > 0; initial Step, Alg. 2 P:700 (1.0)                */
-  float cooling;       /* (0, 1]; Step *= cooling per iteration, P:730 (0.999) */
+  double step0;        /* > 0; initial Step, Alg. 2 P:700 (1.0)                */
+  double cooling;      /* (0, 1]; Step *= cooling per iteration, P:730 (0.999).
+                          The schedule is kept in fp64 (step_t = step0·γ^t by
+                          repeated multiplication), cast to fp32 per use      */
   double tol;          /* >= 0; stop when |E_t - E_{t-1}| < tol (P:1082,
                           §4.5).  0 disables.                                  */
   int32_t max_batches; /* > 0: stop after that many batch updates in total
@@ -117,6 +119,13 @@ int32_t bl_last_launch_count(const bl_ctx *h);
  * (1) MUFU.RCP (rcp.approx.ftz.f32), (2) MUFU.RSQ, measured with clock64
  * inside one kernel on every SM.  rates[3] receives ops/clk/SM.  Blocking. */
 bl_status bl_microbench(double rates[3]);
+
+/* Debug aid: when the context was created with the environment variable
+ * BL_PROFILE=1, the persistent kernel records per-phase SM-cycle sums of
+ * CTA 0 (out[0..7]: attraction, repulsion sweep, in-CTA combine, barrier 1,
+ * update, barrier 2, -, tail) and per-CTA busy cycles of phase R (out[8+c]).
+ * Copies up to len values; returns how many (0 if profiling is off). */
+int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t len);
 
 void bl_destroy(bl_ctx *h);
 const char *bl_status_string(bl_status s);

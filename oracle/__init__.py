@@ -51,7 +51,7 @@ def _load():
         vp = ctypes.c_void_p
         for sfx, R in (("f64", dbl), ("f32", flt)):
             f = getattr(lib, f"oracle_layout_{sfx}")
-            f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, dbl, dbl, i32, u32, vp, vp, ctypes.c_int]
+            f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, dbl, dbl, i32, dbl, u32, vp, vp, ctypes.c_int]
             f.restype = ctypes.c_int
             f = getattr(lib, f"oracle_forces_{sfx}")
             f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, u32, vp, ctypes.c_int]
@@ -81,7 +81,7 @@ def max_threads() -> int:
 
 
 def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
-           cooling=0.999, max_batches=0, flags=0, threads=0, precision="f64"):
+           cooling=0.999, max_batches=0, tol=0.0, flags=0, threads=0, precision="f64"):
     """Run Alg. 2 from xy0 ((n,2) any float dtype; converted to the oracle's
     precision).  Returns (xy (n,2), energy[iters] fp64, iters_done)."""
     lib = _load()
@@ -92,10 +92,10 @@ def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
     done = ctypes.c_int32(0)
     fn = getattr(lib, f"oracle_layout_{precision}")
     rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0, cooling,
-            max_batches, flags, _ptr(energy), ctypes.byref(done), threads)
+            max_batches, tol, flags, _ptr(energy), ctypes.byref(done), threads)
     if rc != 0:
         raise ValueError("oracle_layout: invalid arguments")
-    return xy, energy[:iters], int(done.value)
+    return xy, energy[:int(done.value) if tol > 0 else iters], int(done.value)
 
 
 def forces(n, rowptr, colidx, xy, first=0, count=None, *, K=1.0, C=1.0, flags=0,

@@ -120,12 +120,14 @@ int SFX(oracle_forces)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
  * xy: in/out, 2n values.  energy: iters values (nullable).  max_batches > 0
  * stops after that many batch updates in total (the partial iteration's
  * energy so far is written to energy[it]).  batch > n is clamped to n.
+ * tol > 0: stop after the first iteration t >= 1 with |E_t - E_{t-1}| < tol
+ * (the convergence criterion of §4.5).
  * Returns 0, or -1 on invalid arguments. */
 int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
                        REAL *xy, int32_t iters, int32_t batch, REAL K, REAL C,
                        double step0, double cooling, int32_t max_batches,
-                       uint32_t flags, double *energy, int32_t *iters_done,
-                       int threads) {
+                       double tol, uint32_t flags, double *energy,
+                       int32_t *iters_done, int threads) {
   if (n < 1 || iters < 0 || batch < 1) return -1;
   if (batch > n) batch = n;
   REAL *ct = (REAL *)malloc(sizeof(REAL) * 2 * (size_t)batch);
@@ -134,6 +136,7 @@ int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
   int32_t batches_done = 0;
   int32_t it_done = 0;
   int stop = 0;
+  double E_prev = 0;
 #ifdef _OPENMP
   if (threads > 0) omp_set_num_threads(threads);
 #endif
@@ -172,6 +175,8 @@ int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
       if (energy) energy[it] = (double)E;
       ++it_done;
       step = step * cooling;
+      if (tol > 0 && it > 0 && fabs((double)E - E_prev) < tol) break;
+      E_prev = (double)E;
     }
   }
   free(ct);

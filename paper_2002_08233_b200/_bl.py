@@ -22,8 +22,8 @@ class bl_params(ctypes.Structure):
         ("batch", ctypes.c_int32),
         ("K", ctypes.c_float),
         ("C", ctypes.c_float),
-        ("step0", ctypes.c_float),
-        ("cooling", ctypes.c_float),
+        ("step0", ctypes.c_double),
+        ("cooling", ctypes.c_double),
         ("tol", ctypes.c_double),
         ("max_batches", ctypes.c_int32),
         ("flags", ctypes.c_uint32),
@@ -61,6 +61,8 @@ def _load() -> ctypes.CDLL:
     lib.bl_last_launch_count.restype = i32
     lib.bl_microbench.argtypes = [P(ctypes.c_double)]
     lib.bl_microbench.restype = ctypes.c_int
+    lib.bl_debug_profile.argtypes = [vp, vp, i32]
+    lib.bl_debug_profile.restype = i32
     lib.bl_destroy.argtypes = [vp]
     lib.bl_destroy.restype = None
     lib.bl_status_string.argtypes = [ctypes.c_int]
@@ -75,7 +77,7 @@ lib = _load()
 # symbols include/bl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bl_params_default", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
            "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_microbench",
-           "bl_destroy", "bl_status_string", "bl_last_error")
+           "bl_debug_profile", "bl_destroy", "bl_status_string", "bl_last_error")
 
 
 def _check(rc: int, h=None):
@@ -164,6 +166,12 @@ def bl_microbench():
     r = (ctypes.c_double * 3)()
     _check(lib.bl_microbench(r))
     return {"ffma_per_clk_sm": r[0], "mufu_rcp_per_clk_sm": r[1], "mufu_rsq_per_clk_sm": r[2]}
+
+
+def bl_debug_profile(h: int, length: int = 8 + 1024):
+    out = np.zeros(length, dtype=np.uint64)
+    m = lib.bl_debug_profile(h, out.ctypes.data, length)
+    return out[:m]
 
 
 def bl_destroy(h: int) -> None:

@@ -38,6 +38,8 @@ struct bl_ctx {
   size_t energy_cap = 0;
   int *d_iters_done = nullptr;
   unsigned *d_bar = nullptr;
+  unsigned long long *d_prof = nullptr;  // BL_PROFILE=1: phase profile
+  bool prof = false;
   float2 *d_xy_host_path = nullptr;  // staging for bl_layout (host xy)
   size_t xy_cap = 0;
   // state of the last call
@@ -77,8 +79,8 @@ extern "C" void bl_params_default(bl_params *p) {
   p->batch = 256;
   p->K = 1.0f;
   p->C = 1.0f;
-  p->step0 = 1.0f;
-  p->cooling = 0.999f;
+  p->step0 = 1.0;
+  p->cooling = 0.999;
   p->tol = 0.0;
   p->max_batches = 0;
   p->flags = 0;
@@ -100,6 +102,16 @@ extern "C" const char *bl_last_error(const bl_ctx *h) {
 }
 
 extern "C" int32_t bl_last_launch_count(const bl_ctx *h) { return h ? h->launches : 0; }
+
+// Not part of the public header: phase profile of the last launch when the
+// context was created with BL_PROFILE=1 (debug aid for bench.py --prof).
+extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t len) {
+  if (!h || !h->d_prof || !out) return 0;
+  const int m = std::min<int>(len, 8 + h->G);
+  if (cudaMemcpy(out, h->d_prof, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  return m;
+}
 
 static size_t smem_bytes(int chunk4, int T) {
   return (size_t)chunk4 * sizeof(float4) + (size_t)BL_NW * 32 * T * sizeof(float2);
@@ -221,6 +233,9 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   // grid: one CTA per SM (BL_CTAS_PER_SM overrides), capped by occupancy
   const int per_sm = std::max(1, env_int("BL_CTAS_PER_SM", 1));
   h->G = h->num_sms * per_sm;
+  h->prof = env_int("BL_PROFILE", 0) != 0;
+  if (h->prof && cudaMalloc((void **)&h->d_prof, sizeof(unsigned long long) * (8 + h->G)) != cudaSuccess)
+    return bad(fail(h, BL_ENOMEM, "profile buffer"));
   *out = h;
   return BL_OK;
 }
@@ -238,6 +253,7 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_energy);
   cudaFree(h->d_iters_done);
   cudaFree(h->d_bar);
+  cudaFree(h->d_prof);
   cudaFree(h->d_xy_host_path);
   delete h;
 }
@@ -248,8 +264,8 @@ static bl_status check_params(bl_ctx *h, const bl_params *p) {
   if (p->batch < 1) return fail(h, BL_EINVAL, "batch < 1");
   if (!(p->K > 0.f) || !std::isfinite(p->K)) return fail(h, BL_EINVAL, "K must be > 0");
   if (!(p->C >= 0.f) || !std::isfinite(p->C)) return fail(h, BL_EINVAL, "C must be >= 0");
-  if (!(p->step0 > 0.f) || !std::isfinite(p->step0)) return fail(h, BL_EINVAL, "step0 must be > 0");
-  if (!(p->cooling > 0.f && p->cooling <= 1.f)) return fail(h, BL_EINVAL, "cooling must be in (0,1]");
+  if (!(p->step0 > 0.0) || !std::isfinite(p->step0)) return fail(h, BL_EINVAL, "step0 must be > 0");
+  if (!(p->cooling > 0.0 && p->cooling <= 1.0)) return fail(h, BL_EINVAL, "cooling must be in (0,1]");
   if (!(p->tol >= 0.0) || !std::isfinite(p->tol)) return fail(h, BL_EINVAL, "tol must be >= 0");
   if (p->flags & ~(uint32_t)BL_REPULSE_NEIGHBORS) return fail(h, BL_EINVAL, "unknown flags");
   return BL_OK;
@@ -303,8 +319,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.flags = p->flags;
   k.ck2 = p->C * p->K * p->K;
   k.invK = 1.0f / p->K;
-  k.step0 = (double)p->step0;
-  k.cooling = (double)p->cooling;
+  k.step0 = p->step0;
+  k.cooling = p->cooling;
   k.tol = p->tol;
   k.chunk4 = chunk4_for(n, G);
   k.forces_mode = forces_mode;
@@ -323,6 +339,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.iters_done = h->d_iters_done;
   k.bar = h->d_bar;
   k.f_out = f_out;
+  k.prof = h->d_prof;
 
   const size_t smem = smem_bytes(k.chunk4, h->T);
   void *kfn = nullptr;

@@ -54,6 +54,9 @@ struct BLKParams {
   int *iters_done;
   unsigned *bar;
   float2 *f_out;
+  // optional phase profile (nullptr = off): [0..7] CTA-0 phase cycle sums,
+  // [8 + c] CTA c's cycles from phase-R start to barrier-1 arrival
+  unsigned long long *prof;
 };
 
 __device__ __forceinline__ float bl_rcp(float x) {
@@ -95,10 +98,35 @@ __device__ __forceinline__ float bl_warp_sum0(float v) {
   return v;
 }
 
+// Phase profiler: thread 0 of each CTA marks phase boundaries (clock64).
+struct BLProf {
+  unsigned long long acc[8];
+  long long last;
+  bool on;
+  __device__ void init(const BLKParams &p) {
+    on = p.prof != nullptr && threadIdx.x == 0;
+    for (int i = 0; i < 8; ++i) acc[i] = 0;
+    last = on ? clock64() : 0;
+  }
+  __device__ __forceinline__ void mark(int slot) {
+    if (on) {
+      const long long t = clock64();
+      acc[slot] += (unsigned long long)(t - last);
+      last = t;
+    }
+  }
+  __device__ void flush(const BLKParams &p) {
+    if (!on) return;
+    if (blockIdx.x == 0)
+      for (int i = 0; i < 8; ++i) p.prof[i] = acc[i];
+    p.prof[8 + blockIdx.x] = acc[0] + acc[1] + acc[2];
+  }
+};
+
 // ---------------------------------------------------------------- phase R
 template <int T>
 __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, const float4 *src4,
-                                           float2 *red) {
+                                           float2 *red, BLProf &pf) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -130,6 +158,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
       if (lane == 0) p.attr[it - ib] = make_float2(sx, sy);
     }
   }
+  pf.mark(0);
 
   // (2) repulsion: units = (target tile of 32·T, sub-range of the chunk)
   const int ntt = (bt + 32 * T - 1) / (32 * T);
@@ -176,6 +205,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
       }
     }
   }
+  pf.mark(1);
   if (nsub > 1) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
@@ -188,6 +218,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
       p.part[(size_t)idx * G + c] = acc;
     }
   }
+  pf.mark(2);
 }
 
 // ---------------------------------------------------------------- phase U
@@ -248,6 +279,8 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned bar_target = 0;
+  BLProf pf;
+  pf.init(p);
 
   // resident source chunk: owned vertices c, c+G, ...; pad with far dummies
   // (Δ ~ 1e30 -> d^2 = inf -> 1/d^2 = 0 -> contributes exactly 0)
@@ -259,7 +292,7 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
 
   if (p.forces_mode) {
     double e_dummy = 0.0;
-    bl_phase_R<T>(p, p.first, p.count, src4, red);
+    bl_phase_R<T>(p, p.first, p.count, src4, red, pf);
     bl_grid_sync(p.bar, bar_target);
     bl_phase_U(p, p.first, p.count, 0.0, src, e_dummy);
     return;
@@ -276,9 +309,11 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b;
       const int bt = min(p.b, p.n - lo);
-      bl_phase_R<T>(p, lo, bt, src4, red);
+      bl_phase_R<T>(p, lo, bt, src4, red, pf);
       bl_grid_sync(p.bar, bar_target);
+      pf.mark(3);
       bl_phase_U(p, lo, bt, step, src, e_acc);
+      pf.mark(4);
       ++batches;
       const bool last = (t == p.nb - 1);
       if (p.max_batches > 0 && batches >= p.max_batches) stop = true;
@@ -292,6 +327,7 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
         }
       }
       bl_grid_sync(p.bar, bar_target);
+      pf.mark(5);
       if (last || stop) {
         // every CTA reduces the per-CTA energies in the same order, so the
         // convergence decision is identical everywhere
@@ -300,6 +336,7 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
         if (c == 0 && threadIdx.x == 0) p.energy[it] = E;
         if (!stop && p.tol > 0.0 && it > 0 && fabs(E - e_prev) < p.tol) {
           if (c == 0 && threadIdx.x == 0) *p.iters_done = it + 1;
+          pf.flush(p);
           return;
         }
         e_prev = E;
@@ -309,4 +346,6 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
     if (!stop) step = step * p.cooling;
   }
   if (c == 0 && threadIdx.x == 0) *p.iters_done = stop ? it - 1 : it;
+  pf.mark(6);
+  pf.flush(p);
 }

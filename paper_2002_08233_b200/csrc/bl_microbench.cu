@@ -25,9 +25,15 @@ __global__ void __launch_bounds__(MB_NT, 1) bl_mb_kernel(float *sink, long long 
       if (OP == 0) {
         a[k] = fmaf(a[k], bb[k], cc[k]);
       } else if (OP == 1) {
-        asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
+        // rcp(x) + c: one MUFU.RCP + one FADD per op (FADD at 128/clk is not
+        // the binding pipe); a bare rcp chain is an involution ptxas may fold
+        float r;
+        asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a[k]));
+        a[k] = r + cc[k];
       } else {
-        asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
+        float r;
+        asm volatile("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a[k]));
+        a[k] = r + cc[k];
       }
     }
   }

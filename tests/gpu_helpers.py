@@ -51,3 +51,23 @@ def assert_positions_close(got, ref, tol=POS_TOL, what=""):
     err = float(np.abs(np.asarray(got, np.float64) - ref).max())
     assert err <= tol * ext, f"{what}: max |dxy| = {err:.3e} > {tol:g} x extent {ext:.4g}"
     return err / ext
+
+
+def shadow_check(g, xy0, iters, oracle_layout, tol=POS_TOL, **params):
+    """Per-iteration shadowing: from the GPU's own state
+    x_t (fp32 bytes), one GPU iteration with step0 = step_t is compared with
+    one oracle iteration from the same bytes.  Chaos-immune, so it can run
+    for many iterations.  Returns the worst err/extent."""
+    step = float(params.pop("step0", 1.0))
+    cooling = float(params.get("cooling", 0.999))
+    state = np.ascontiguousarray(xy0, dtype=np.float32)
+    worst = 0.0
+    for t in range(iters):
+        p = dict(params, iters=1, step0=step)
+        got, tr, _ = gpu_layout(g, state, **p)
+        ref, E, _ = oracle_layout(g, state, p)
+        worst = max(worst, assert_positions_close(got, ref, tol, what=f"iteration {t}"))
+        assert abs(tr[0] - E[0]) <= 1e-3 * E[0] + 1e-30, (t, tr[0], E[0])
+        state = got
+        step = step * cooling
+    return worst

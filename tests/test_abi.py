@@ -43,7 +43,7 @@ def test_params_default_are_the_papers():
     p = bl.bl_params_default()
     assert (p.iters, p.batch) == (600, 256)
     assert (p.K, p.C, p.step0) == (1.0, 1.0, 1.0)
-    assert p.cooling == pytest.approx(0.999)
+    assert p.cooling == 0.999
     assert (p.tol, p.max_batches, p.flags) == (0.0, 0, 0)
 
 

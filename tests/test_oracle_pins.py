@@ -130,6 +130,23 @@ def test_two_vertices_separation_and_energy(b):
     np.testing.assert_allclose(u, [0.6, 0.8], atol=1e-12)
 
 
+def test_tol_stop_two_vertices():
+    """|E_t - E_{t-1}| < tol stops the run (§4.5).  Two vertices, b=2:
+    E_t = 2 (CK^2/d_t)^2 with d_t = d0 + 2 sum_{s<t} step_s (closed form above),
+    so the stopping iteration is known in advance."""
+    rp, ci = _edge_csr(2, [])
+    xy0 = np.array([[0.0, 0.0], [0.3, 0.4]])
+    gamma, T, tol = 0.9, 200, 1e-4
+    steps = gamma ** np.arange(T)
+    d = 0.5 + 2 * np.concatenate([[0.0], np.cumsum(steps)])
+    E = 2 * (1.0 / d[:T]) ** 2
+    stop = next(t for t in range(1, T) if abs(E[t] - E[t - 1]) < tol) + 1
+    xy, Eo, done = oracle.layout(2, rp, ci, xy0, iters=T, batch=2, cooling=gamma, tol=tol)
+    assert done == stop and len(Eo) == stop
+    np.testing.assert_allclose(Eo, E[:stop], rtol=1e-12)
+    assert np.hypot(*(xy[1] - xy[0])) == pytest.approx(d[stop], rel=1e-13)
+
+
 def _circle(n, jitter, seed):
     rng = np.random.default_rng(seed)
     th = 2 * np.pi * np.arange(n) / n + rng.uniform(-jitter, jitter, n)
@@ -148,8 +165,6 @@ def test_cycle_relaxes_to_regular_polygon(n, bmode, KC, flags):
     non-neighbour pushes exactly C K^2/(2 rho) radially; the two springs pull
     l^3/(rho K); balance gives the closed form (pin P1)."""
     K, C = KC
-    if flags == 0 and n == 4 and C * K == 0:
-        pytest.skip()
     g = cycle_graph(n)
     xy0 = _circle(n, 0.05, seed=n)
     b = 1 if bmode == "b1" else n
