@@ -115,10 +115,11 @@ int32_t bl_max_vertices(void);
 int32_t bl_last_launch_count(const bl_ctx *h);
 
 /* Microbenchmark of the roofline denominators on the current device:
- * sustained warp-instruction rates per SM per clock of (0) 3-register FFMA,
- * (1) MUFU.RCP (rcp.approx.ftz.f32), (2) MUFU.RSQ, measured with clock64
- * inside one kernel on every SM.  rates[3] receives ops/clk/SM.  Blocking. */
-bl_status bl_microbench(double rates[3]);
+ * sustained thread-op rates per SM per clock of (0) 3-register FFMA,
+ * (1) MUFU.RCP (rcp.approx.ftz.f32), (2) MUFU.RSQ, (3) packed FFMA2
+ * (fma.rn.f32x2, 2 ops per lane), measured with clock64 inside one kernel on
+ * every SM.  rates[4] receives ops/clk/SM.  Blocking. */
+bl_status bl_microbench(double rates[4]);
 
 /* Debug aid: when the context was created with the environment variable
  * BL_PROFILE=1, the persistent kernel records per-phase SM-cycle sums of

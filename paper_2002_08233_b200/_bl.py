@@ -163,9 +163,10 @@ def bl_last_launch_count(h: int) -> int:
 
 
 def bl_microbench():
-    r = (ctypes.c_double * 3)()
+    r = (ctypes.c_double * 4)()
     _check(lib.bl_microbench(r))
-    return {"ffma_per_clk_sm": r[0], "mufu_rcp_per_clk_sm": r[1], "mufu_rsq_per_clk_sm": r[2]}
+    return {"ffma_per_clk_sm": r[0], "mufu_rcp_per_clk_sm": r[1], "mufu_rsq_per_clk_sm": r[2],
+            "ffma2_lane_ops_per_clk_sm": r[3]}
 
 
 def bl_debug_profile(h: int, length: int = 8 + 1024):

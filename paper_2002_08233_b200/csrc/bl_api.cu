@@ -18,11 +18,19 @@
 #include "../../include/bl.h"
 #include "bl_kernel.cuh"
 
+#ifndef BL_DEFAULT_T
+#define BL_DEFAULT_T 4
+#endif
+#ifndef BL_DEFAULT_TP
+#define BL_DEFAULT_TP 0
+#endif
+
 struct bl_ctx {
   int32_t n = 0, nnz = 0;
   int device = 0, num_sms = 0;
   int G = 0;  // grid size of the persistent kernel
   int T = 4;  // register-blocked targets per thread
+  int TP = 0; // of which use the paired reciprocal (bl_sweep)
   // device CSR + items
   int *d_rowptr = nullptr, *d_colidx = nullptr;
   int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
@@ -113,9 +121,7 @@ extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t 
   return m;
 }
 
-static size_t smem_bytes(int chunk4, int T) {
-  return (size_t)chunk4 * sizeof(float4) + (size_t)BL_NW * 32 * T * sizeof(float2);
-}
+static size_t smem_bytes(int chunk4, int T) { return bl_smem_bytes(chunk4, T); }
 
 static int chunk4_for(int n, int G) {
   const int per = (n + G - 1) / G;  // owned sources per CTA (max)
@@ -127,10 +133,21 @@ static int env_int(const char *name, int def) {
   return (s && *s) ? atoi(s) : def;
 }
 
-template <int T>
-static cudaError_t set_smem_attr(size_t bytes) {
-  return cudaFuncSetAttribute(bl_layout_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)bytes);
+// Kernel variants (T targets per thread, TP of them paired-reciprocal).
+struct BLVariant {
+  int T, TP;
+  void *fn;
+};
+#define BL_V(T, TP) {T, TP, (void *)bl_layout_kernel<T, TP>}
+static const BLVariant kVariants[] = {
+    BL_V(2, 0), BL_V(2, 1), BL_V(2, 2), BL_V(4, 0), BL_V(4, 1), BL_V(4, 2),
+    BL_V(4, 3), BL_V(4, 4), BL_V(8, 0), BL_V(8, 2), BL_V(8, 3), BL_V(8, 4),
+};
+#undef BL_V
+static const BLVariant *find_variant(int T, int TP) {
+  for (const auto &v : kVariants)
+    if (v.T == T && v.TP == TP) return &v;
+  return nullptr;
 }
 
 extern "C" int32_t bl_max_vertices(void) {
@@ -139,7 +156,7 @@ extern "C" int32_t bl_max_vertices(void) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return 0;
-  const long long room = (long long)optin - 2048 - (long long)BL_NW * 32 * 8 * sizeof(float2);
+  const long long room = (long long)optin - 2048 - (long long)bl_smem_bytes(0, 8);
   const long long per = room / (long long)sizeof(float4) * 2;
   const long long n = per * sms;
   return (int32_t)std::min<long long>(n, 0x7fffffff);
@@ -190,8 +207,12 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   if (cudaGetDevice(&h->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess)
     return bad(fail(h, BL_ECUDA, "no CUDA device"));
-  h->T = env_int("BL_T", 4);
-  if (h->T != 4 && h->T != 8 && h->T != 2) h->T = 4;
+  h->T = env_int("BL_T", BL_DEFAULT_T);
+  h->TP = env_int("BL_TP", BL_DEFAULT_TP);
+  if (!find_variant(h->T, h->TP)) {
+    h->T = BL_DEFAULT_T;
+    h->TP = BL_DEFAULT_TP;
+  }
 
   // attraction items: ceil(deg(v)/ECH) per vertex, in vertex order
   h->item_ptr.assign((size_t)n + 1, 0);
@@ -342,13 +363,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.prof = h->d_prof;
 
   const size_t smem = smem_bytes(k.chunk4, h->T);
-  void *kfn = nullptr;
-  cudaError_t e;
-  switch (h->T) {
-    case 2: e = set_smem_attr<2>(smem); kfn = (void *)bl_layout_kernel<2>; break;
-    case 8: e = set_smem_attr<8>(smem); kfn = (void *)bl_layout_kernel<8>; break;
-    default: e = set_smem_attr<4>(smem); kfn = (void *)bl_layout_kernel<4>; break;
-  }
+  void *kfn = find_variant(h->T, h->TP)->fn;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
   int occ = 0;
   BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, BL_NT, smem));

@@ -35,7 +35,29 @@
 #define BL_NT 512          // threads per CTA (16 warps)
 #define BL_NW (BL_NT / 32)
 #define BL_ECH 128         // CSR entries per attraction item
-#define BL_EPS2 1e-30f     // self/coincident-pair guard folded into d^2
+#define BL_EPS2 1e-20f     // self/coincident-pair guard folded into d^2
+#define BL_UNITS (2 * BL_NW)  // target repulsion work units per CTA per batch
+#define BL_TGT_CAP 4096       // batch targets staged in shared memory (else read from L2)
+#define BL_MIN_UNIT4 16       // minimum float4 (2 sources) per repulsion unit
+
+// Partition of one batch's repulsion work inside a CTA: ntt target tiles of
+// 32·T targets x nsub sub-ranges of the CTA's resident sources.
+struct BLUnits {
+  int ntt, nsub;
+};
+__host__ __device__ inline BLUnits bl_units(int bt, int T, int full4) {
+  BLUnits u;
+  u.ntt = (bt + 32 * T - 1) / (32 * T);
+  int ns = u.ntt >= BL_UNITS ? 1 : BL_UNITS / u.ntt;
+  const int cap = full4 / BL_MIN_UNIT4;
+  if (ns > cap) ns = cap;
+  u.nsub = ns < 1 ? 1 : ns;
+  return u;
+}
+// shared memory: [src4: chunk4 float4][tgt: BL_TGT_CAP float2][red: BL_UNITS·32·T float2]
+__host__ __device__ inline size_t bl_smem_bytes(int chunk4, int T) {
+  return (size_t)chunk4 * 16 + (size_t)BL_TGT_CAP * 8 + (size_t)BL_UNITS * 32 * T * 8;
+}
 
 struct BLKParams {
   int n, b, nb, iters, max_batches;
@@ -69,6 +91,90 @@ __device__ __forceinline__ float bl_rsqrt(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// ---- packed fp32x2 (sm_100a FADD2/FFMA2/FMUL2): two pair evaluations per
+// issue slot.  Operand (a, b) lives in one 64-bit register pair.
+typedef unsigned long long bl_f2;
+__device__ __forceinline__ bl_f2 f2pack(float a, float b) {
+  bl_f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(bl_f2 v, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ bl_f2 f2sub(bl_f2 a, bl_f2 b) {
+  bl_f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ bl_f2 f2fma(bl_f2 a, bl_f2 b, bl_f2 c) {
+  bl_f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ bl_f2 f2mul(bl_f2 a, bl_f2 b) {
+  bl_f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Shared-memory source chunk, two sources per float4 in (x_a, x_b, y_a, y_b)
+// order so that one LDS.128 yields the packed X = (x_a, x_b), Y = (y_a, y_b).
+__device__ __forceinline__ void bl_src_set(float4 *src4, int k, float2 v) {
+  float *f = reinterpret_cast<float *>(src4 + (k >> 1));
+  f[k & 1] = v.x;
+  f[2 + (k & 1)] = v.y;
+}
+__device__ __forceinline__ float2 bl_src_get(const float4 *src4, int k) {
+  const float *f = reinterpret_cast<const float *>(src4 + (k >> 1));
+  return make_float2(f[k & 1], f[2 + (k & 1)]);
+}
+
+// The repulsion inner loop: for T register-blocked targets and the sources
+// of src4[s0, s1): R_t += Δ / d^2.  Per (target, float4) = 2 pairs:
+//   DX = X - tx, DY = Y - ty (FADD2 x2), D2 = DX^2 + DY^2 + eps (FFMA2 x2),
+//   INV = 1/D2, R += (DX, DY) * INV (FFMA2 x2).
+// INV: for the first TP targets the two reciprocals share ONE MUFU.RCP:
+//   r = 1/(d2a d2b), INV = (d2b r, d2a r) (FMUL + MUFU + FMUL2), otherwise
+//   two MUFU.RCP.  TP trades SFU work for FP32 work.
+// Requires every D2 lane finite and d2a·d2b a normal float when paired: true
+// for real sources (d^2 >= 1e-20 by the eps fold, < 1e19); dummy (far)
+// sources are only ever swept with TP = 0.
+template <int T, int TP>
+__device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0, int s1,
+                                         const float (&tx)[T], const float (&ty)[T], bl_f2 (&AX)[T],
+                                         bl_f2 (&AY)[T]) {
+  const bl_f2 EPS = f2pack(BL_EPS2, BL_EPS2);
+  bl_f2 TX[T], TY[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    TX[k] = f2pack(tx[k], tx[k]);
+    TY[k] = f2pack(ty[k], ty[k]);
+  }
+#pragma unroll 2
+  for (int s = s0; s < s1; ++s) {
+    const float4 q = src4[s];  // two sources, broadcast to the warp
+    const bl_f2 X = f2pack(q.x, q.y), Y = f2pack(q.z, q.w);
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const bl_f2 DX = f2sub(X, TX[k]);
+      const bl_f2 DY = f2sub(Y, TY[k]);
+      const bl_f2 D2 = f2fma(DX, DX, f2fma(DY, DY, EPS));
+      float a, b;
+      f2unpack(D2, a, b);
+      bl_f2 INV;
+      if (k < TP) {
+        const float r = bl_rcp(a * b);
+        INV = f2mul(f2pack(b, a), f2pack(r, r));
+      } else {
+        INV = f2pack(bl_rcp(a), bl_rcp(b));
+      }
+      AX[k] = f2fma(DX, INV, AX[k]);
+      AY[k] = f2fma(DY, INV, AY[k]);
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned bl_ld_acquire(const unsigned *p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -77,16 +183,19 @@ __device__ __forceinline__ unsigned bl_ld_acquire(const unsigned *p) {
 
 // Sense-free monotone grid barrier: the counter only grows; barrier k of a
 // launch completes when it reaches k·G.  Requires co-residency (cooperative
-// launch).  Thread 0 fences the CTA's writes (gpu scope) before arriving.
-__device__ __forceinline__ void bl_grid_sync(unsigned *bar, unsigned &target) {
+// launch).  After the CTA barrier, thread 0 publishes the CTA's writes with a
+// gpu-scope acq_rel fence + relaxed reduction, then spins with acquire loads
+// (the arrive/wait pattern of CUTLASS's GenericBarrier).  Thread 0 also
+// resets the CTA's dynamic work counter for the next phase.
+__device__ __forceinline__ void bl_grid_sync(unsigned *bar, unsigned &target, int *unit_ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     target += gridDim.x;
-    __threadfence();
-    atomicAdd(bar, 1u);
+    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar)
+                 : "memory");
+    *unit_ctr = 0;
     while ((int)(bl_ld_acquire(bar) - target) < 0) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -124,11 +233,16 @@ struct BLProf {
 };
 
 // ---------------------------------------------------------------- phase R
-template <int T>
+template <int T, int TP>
 __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, const float4 *src4,
-                                           float2 *red, BLProf &pf) {
+                                           float2 *tgt, float2 *red, int *unit_ctr, BLProf &pf) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool tgt_smem = bt <= BL_TGT_CAP;
+
+  // (0) stage the batch's targets (frozen coordinates)
+  if (tgt_smem)
+    for (int i = threadIdx.x; i < bt; i += BL_NT) tgt[i] = __ldcg(p.xy + lo + i);
 
   // (1) attraction items of this batch, spread over all warps of the grid
   {
@@ -159,59 +273,64 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
     }
   }
   pf.mark(0);
+  __syncthreads();  // targets staged
 
-  // (2) repulsion: units = (target tile of 32·T, sub-range of the chunk)
-  const int ntt = (bt + 32 * T - 1) / (32 * T);
-  const int nsub = ntt <= BL_NW ? BL_NW / ntt : 1;
-  const int nunits = ntt * nsub;
-  for (int u = warp; u < nunits; u += BL_NW) {
-    const int tile = u % ntt, sub = u / ntt;
-    const int s0 = (int)(((long long)p.chunk4 * sub) / nsub);
-    const int s1 = (int)(((long long)p.chunk4 * (sub + 1)) / nsub);
-    float tx[T], ty[T], ax[T], ay[T];
+  // (2) repulsion: units = (target tile of 32·T, sub-range of the CTA's
+  // resident sources), grabbed dynamically by warps (warps that did
+  // attraction items take fewer).  Each unit's result has its own slot and
+  // the slots are combined in a fixed order, so the result does not depend
+  // on which warp ran which unit.
+  // CTA c owns m_c = ceil((n - c)/G) sources: full4 float4s of two real
+  // sources (swept with pairing), then at most one float4 holding one real
+  // source and one far dummy (swept unpaired, by the last sub-range).
+  const int m_c = c < p.n ? (p.n - 1 - c) / G + 1 : 0;
+  const int full4 = m_c >> 1;
+  const BLUnits U = bl_units(bt, T, full4);
+  const int nunits = U.ntt * U.nsub;
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(unit_ctr, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nunits) break;
+    const int tile = u % U.ntt, sub = u / U.ntt;
+    const int s0 = (int)(((long long)full4 * sub) / U.nsub);
+    const int s1 = (int)(((long long)full4 * (sub + 1)) / U.nsub);
+    float tx[T], ty[T];
+    bl_f2 AX[T], AY[T];
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       const int idx = tile * 32 * T + k * 32 + lane;
       float2 t = make_float2(0.f, 0.f);
-      if (idx < bt) t = __ldcg(p.xy + lo + idx);
+      if (idx < bt) t = tgt_smem ? tgt[idx] : __ldcg(p.xy + lo + idx);
       tx[k] = t.x;
       ty[k] = t.y;
-      ax[k] = 0.f;
-      ay[k] = 0.f;
+      AX[k] = f2pack(0.f, 0.f);
+      AY[k] = f2pack(0.f, 0.f);
     }
-#pragma unroll 2
-    for (int s = s0; s < s1; ++s) {
-      const float4 q = src4[s];  // two sources, broadcast to the warp
-#pragma unroll
-      for (int k = 0; k < T; ++k) {
-        const float dx0 = q.x - tx[k], dy0 = q.y - ty[k];
-        const float dx1 = q.z - tx[k], dy1 = q.w - ty[k];
-        const float r0 = bl_rcp(fmaf(dx0, dx0, fmaf(dy0, dy0, BL_EPS2)));
-        const float r1 = bl_rcp(fmaf(dx1, dx1, fmaf(dy1, dy1, BL_EPS2)));
-        ax[k] = fmaf(dx0, r0, ax[k]);
-        ay[k] = fmaf(dy0, r0, ay[k]);
-        ax[k] = fmaf(dx1, r1, ax[k]);
-        ay[k] = fmaf(dy1, r1, ay[k]);
-      }
-    }
+    bl_sweep<T, TP>(src4, s0, s1, tx, ty, AX, AY);
+    if ((m_c & 1) && sub == U.nsub - 1) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       const int idx = tile * 32 * T + k * 32 + lane;
+      float ax0, ax1, ay0, ay1;
+      f2unpack(AX[k], ax0, ax1);
+      f2unpack(AY[k], ay0, ay1);
+      const float2 r = make_float2(ax0 + ax1, ay0 + ay1);
       if (idx < bt) {
-        if (nsub == 1)
-          p.part[(size_t)idx * G + c] = make_float2(ax[k], ay[k]);
+        if (U.nsub == 1)
+          p.part[(size_t)idx * G + c] = r;
         else
-          red[sub * (ntt * 32 * T) + idx] = make_float2(ax[k], ay[k]);
+          red[sub * (U.ntt * 32 * T) + idx] = r;
       }
     }
   }
   pf.mark(1);
-  if (nsub > 1) {
+  if (U.nsub > 1) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
       float2 acc = red[idx];
-      for (int s = 1; s < nsub; ++s) {
-        const float2 v = red[s * (ntt * 32 * T) + idx];
+      for (int s = 1; s < U.nsub; ++s) {
+        const float2 v = red[s * (U.ntt * 32 * T) + idx];
         acc.x += v.x;
         acc.y += v.y;
       }
@@ -223,31 +342,37 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
 
 // ---------------------------------------------------------------- phase U
 // Owner CTA c handles v in [lo, lo+bt) with v ≡ c (mod G); warp w takes the
-// w-th, (w+NW)-th, ... of them.  Returns nothing; accumulates e_acc (lane 0).
+// w-th, (w+NW)-th, ... of them.  All loads of one vertex are issued before
+// any is consumed (one L2 round trip for the partials + item bounds, one for
+// the attraction items).  Accumulates ||f||^2 into e_acc (lane 0).
 __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, double stepd,
-                                           float2 *src, double &e_acc) {
+                                           float4 *src4, double &e_acc) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v0 = lo + ((c - lo % G) + G) % G;
   const int ib = __ldg(p.item_ptr + lo);
   for (int v = v0 + warp * G; v < lo + bt; v += BL_NW * G) {
     const int local = v - lo;
+    const int a0 = __ldg(p.item_ptr + v) - ib, a1 = __ldg(p.item_ptr + v + 1) - ib;
+    const float2 *row = p.part + (size_t)local * G;
     float rx = 0.f, ry = 0.f;
+#pragma unroll 8
     for (int cc = lane; cc < G; cc += 32) {
-      const float2 q = __ldcg(p.part + (size_t)local * G + cc);
+      const float2 q = __ldcg(row + cc);
       rx += q.x;
       ry += q.y;
     }
+    float sx = 0.f, sy = 0.f;
+    for (int a = a0 + lane; a < a1; a += 32) {
+      const float2 q = __ldcg(p.attr + a);
+      sx += q.x;
+      sy += q.y;
+    }
     rx = bl_warp_sum0(rx);
     ry = bl_warp_sum0(ry);
+    sx = bl_warp_sum0(sx);
+    sy = bl_warp_sum0(sy);
     if (lane == 0) {
-      float sx = 0.f, sy = 0.f;
-      const int a0 = __ldg(p.item_ptr + v), a1 = __ldg(p.item_ptr + v + 1);
-      for (int a = a0; a < a1; ++a) {
-        const float2 q = __ldcg(p.attr + (a - ib));
-        sx += q.x;
-        sy += q.y;
-      }
       const float fx = fmaf(-p.ck2, rx, sx);
       const float fy = fmaf(-p.ck2, ry, sy);
       if (p.forces_mode) {
@@ -256,11 +381,11 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
         const double q = (double)fx * fx + (double)fy * fy;
         if (q > 0.0) {
           const double s = stepd / sqrt(q);
-          float2 cv = src[(v - c) / G];  // the owner's resident copy of xy[v]
+          float2 cv = bl_src_get(src4, (v - c) / G);  // the owner's resident copy of xy[v]
           cv.x = (float)((double)cv.x + s * fx);
           cv.y = (float)((double)cv.y + s * fy);
           p.xy[v] = cv;
-          src[(v - c) / G] = cv;
+          bl_src_set(src4, (v - c) / G, cv);
         }
         e_acc += q;
       }
@@ -268,13 +393,15 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
   }
 }
 
-template <int T>
+template <int T, int TP>
 __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   extern __shared__ float4 bl_smem[];
   float4 *src4 = bl_smem;
-  float2 *src = reinterpret_cast<float2 *>(bl_smem);
-  float2 *red = reinterpret_cast<float2 *>(bl_smem + p.chunk4);
+  float2 *tgt = reinterpret_cast<float2 *>(bl_smem + p.chunk4);
+  float2 *red = tgt + BL_TGT_CAP;
   __shared__ double e_warp[BL_NW];
+  __shared__ int unit_ctr;
+  if (threadIdx.x == 0) unit_ctr = 0;
 
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -286,15 +413,15 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   // (Δ ~ 1e30 -> d^2 = inf -> 1/d^2 = 0 -> contributes exactly 0)
   for (int k = threadIdx.x; k < 2 * p.chunk4; k += BL_NT) {
     const long long v = (long long)c + (long long)k * G;
-    src[k] = v < p.n ? __ldcg(p.xy + v) : make_float2(1e30f, 1e30f);
+    bl_src_set(src4, k, v < p.n ? __ldcg(p.xy + v) : make_float2(1e30f, 1e30f));
   }
   __syncthreads();
 
   if (p.forces_mode) {
     double e_dummy = 0.0;
-    bl_phase_R<T>(p, p.first, p.count, src4, red, pf);
-    bl_grid_sync(p.bar, bar_target);
-    bl_phase_U(p, p.first, p.count, 0.0, src, e_dummy);
+    bl_phase_R<T, TP>(p, p.first, p.count, src4, tgt, red, &unit_ctr, pf);
+    bl_grid_sync(p.bar, bar_target, &unit_ctr);
+    bl_phase_U(p, p.first, p.count, 0.0, src4, e_dummy);
     return;
   }
 
@@ -309,10 +436,10 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b;
       const int bt = min(p.b, p.n - lo);
-      bl_phase_R<T>(p, lo, bt, src4, red, pf);
-      bl_grid_sync(p.bar, bar_target);
+      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, &unit_ctr, pf);
+      bl_grid_sync(p.bar, bar_target, &unit_ctr);
       pf.mark(3);
-      bl_phase_U(p, lo, bt, step, src, e_acc);
+      bl_phase_U(p, lo, bt, step, src4, e_acc);
       pf.mark(4);
       ++batches;
       const bool last = (t == p.nb - 1);
@@ -326,7 +453,7 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
           p.e_cta[(it & 1) * G + c] = e;
         }
       }
-      bl_grid_sync(p.bar, bar_target);
+      bl_grid_sync(p.bar, bar_target, &unit_ctr);
       pf.mark(5);
       if (last || stop) {
         // every CTA reduces the per-CTA energies in the same order, so the

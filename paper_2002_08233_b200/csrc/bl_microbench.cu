@@ -30,10 +30,18 @@ __global__ void __launch_bounds__(MB_NT, 1) bl_mb_kernel(float *sink, long long 
         float r;
         asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a[k]));
         a[k] = r + cc[k];
-      } else {
+      } else if (OP == 2) {
         float r;
         asm volatile("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a[k]));
         a[k] = r + cc[k];
+      } else if (k < 4) {
+        // packed FFMA2 on (a[k], a[k+4]): counts as 2 thread-ops
+        unsigned long long v, m, c2;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(a[k]), "f"(a[k + 4]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "f"(bb[k]), "f"(bb[k + 4]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(c2) : "f"(cc[k]), "f"(cc[k + 4]));
+        asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(v) : "l"(v), "l"(m), "l"(c2));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(a[k]), "=f"(a[k + 4]) : "l"(v));
       }
     }
   }
@@ -46,7 +54,7 @@ __global__ void __launch_bounds__(MB_NT, 1) bl_mb_kernel(float *sink, long long 
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
-extern "C" bl_status bl_microbench(double rates[3]) {
+extern "C" bl_status bl_microbench(double rates[4]) {
   if (!rates) return BL_EINVAL;
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return BL_ECUDA;
@@ -60,11 +68,12 @@ extern "C" bl_status bl_microbench(double rates[3]) {
   }
   long long *h = new long long[sms];
   bl_status st = BL_OK;
-  for (int op = 0; op < 3 && st == BL_OK; ++op) {
+  for (int op = 0; op < 4 && st == BL_OK; ++op) {
     for (int rep = 0; rep < 2; ++rep) {  // first pass warms clocks
       if (op == 0) bl_mb_kernel<0><<<sms, MB_NT>>>(sink, cyc, 1.0f);
       if (op == 1) bl_mb_kernel<1><<<sms, MB_NT>>>(sink, cyc, 1.0f);
       if (op == 2) bl_mb_kernel<2><<<sms, MB_NT>>>(sink, cyc, 1.0f);
+      if (op == 3) bl_mb_kernel<3><<<sms, MB_NT>>>(sink, cyc, 1.0f);
     }
     if (cudaDeviceSynchronize() != cudaSuccess ||
         cudaMemcpy(h, cyc, sms * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess) {
