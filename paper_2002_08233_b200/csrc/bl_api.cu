@@ -39,6 +39,8 @@ struct bl_ctx {
   // scratch
   float2 *d_part = nullptr;
   size_t part_cap = 0;  // float2 elements
+  float2 *d_pend = nullptr;
+  size_t pend_cap = 0;
   float2 *d_attr = nullptr;
   size_t attr_cap = 0;
   double *d_e_cta = nullptr;
@@ -270,6 +272,7 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_item_k0);
   cudaFree(h->d_part);
   cudaFree(h->d_attr);
+  cudaFree(h->d_pend);
   cudaFree(h->d_e_cta);
   cudaFree(h->d_energy);
   cudaFree(h->d_iters_done);
@@ -321,7 +324,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   const int b = forces_mode ? std::max(1, count) : std::min(p->batch, n);
   const int G = h->G;
   bl_status s;
-  if ((s = grow(h, h->d_part, h->part_cap, (size_t)b * G)) != BL_OK) return s;
+  if ((s = grow(h, h->d_part, h->part_cap, (size_t)2 * b * G)) != BL_OK) return s;
+  if ((s = grow(h, h->d_pend, h->pend_cap, (size_t)2 * b)) != BL_OK) return s;
   const int mi = forces_mode ? max_items_per_batch(h, b, first, count)
                              : max_items_per_batch(h, b, 0, n);
   if ((s = grow(h, h->d_attr, h->attr_cap, (size_t)mi)) != BL_OK) return s;
@@ -354,6 +358,12 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.item_v = h->d_item_v;
   k.item_k0 = h->d_item_k0;
   k.part = h->d_part;
+  k.pend = h->d_pend;
+  // one barrier per batch needs >= 4 batches per iteration,
+  // targets within the staging buffer, an even batch and 16-byte aligned
+  // coordinates (16-byte cp.async of target pairs)
+  k.pipelined = !forces_mode && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 && (((uintptr_t)d_xy) & 15) == 0 &&
+                env_int("BL_PIPELINE", 1) != 0;
   k.attr = h->d_attr;
   k.e_cta = h->d_e_cta;
   k.energy = h->d_energy;

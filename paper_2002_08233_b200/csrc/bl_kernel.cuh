@@ -54,9 +54,9 @@ __host__ __device__ inline BLUnits bl_units(int bt, int T, int full4) {
   u.nsub = ns < 1 ? 1 : ns;
   return u;
 }
-// shared memory: [src4: chunk4 float4][tgt: BL_TGT_CAP float2][red: BL_UNITS·32·T float2]
+// shared memory: [src4: chunk4 float4][tgt: 2 x BL_TGT_CAP float2][red: BL_UNITS·32·T float2]
 __host__ __device__ inline size_t bl_smem_bytes(int chunk4, int T) {
-  return (size_t)chunk4 * 16 + (size_t)BL_TGT_CAP * 8 + (size_t)BL_UNITS * 32 * T * 8;
+  return (size_t)chunk4 * 16 + (size_t)2 * BL_TGT_CAP * 8 + (size_t)BL_UNITS * 32 * T * 8;
 }
 
 struct BLKParams {
@@ -69,7 +69,9 @@ struct BLKParams {
   float2 *xy;
   const int *rowptr, *colidx;
   const int *item_ptr, *item_v, *item_k0;
-  float2 *part;          // [b][G]
+  float2 *part;          // [2][b][G] (pipelined path double-buffers by batch parity)
+  float2 *pend;          // [2][b]   new coordinates of the last two batches (pipelined)
+  int pipelined;         // 1: one grid barrier per batch (needs nb >= 4)
   float2 *attr;          // [max items per batch]
   double *e_cta;         // [2][G]
   double *energy;        // [iters]
@@ -187,13 +189,15 @@ __device__ __forceinline__ unsigned bl_ld_acquire(const unsigned *p) {
 // gpu-scope acq_rel fence + relaxed reduction, then spins with acquire loads
 // (the arrive/wait pattern of CUTLASS's GenericBarrier).  Thread 0 also
 // resets the CTA's dynamic work counter for the next phase.
-__device__ __forceinline__ void bl_grid_sync(unsigned *bar, unsigned &target, int *unit_ctr) {
+__device__ __forceinline__ void bl_grid_sync(unsigned *bar, unsigned &target, int *unit_ctr,
+                                             int *u_done = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     target += gridDim.x;
     asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar)
                  : "memory");
     *unit_ctr = 0;
+    if (u_done) *u_done = 0;
     while ((int)(bl_ld_acquire(bar) - target) < 0) {
     }
   }
@@ -231,6 +235,102 @@ struct BLProf {
     p.prof[8 + blockIdx.x] = acc[0] + acc[1] + acc[2];
   }
 };
+
+// The repulsion work of one batch inside a CTA, as dynamically grabbed
+// units = (target tile of 32·T, sub-range of the CTA's resident sources).
+// Warps that did other work first (attraction items, updates) take fewer
+// units.  Each unit's result has its own slot and the slots are combined in
+// a fixed order, so the result does not depend on which warp ran which unit.
+// CTA c owns m_c = ceil((n - c)/G) sources: full4 float4s of two real
+// sources (swept with pairing), then at most one float4 holding one real
+// source and one far dummy (swept unpaired, by the last sub-range).
+// Units whose source range meets the float4 range [d_lo, d_hi) ("dirty":
+// being updated by this CTA's own update warps in the same phase) are
+// grabbed last and wait until *u_done reaches u_need.
+// tgt: staged targets in shared memory, or nullptr to read them from L2.
+template <int T, int TP>
+__device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int bt,
+                                               const float4 *src4, const float2 *tgt, float2 *red,
+                                               int *unit_ctr, float2 *part, int d_lo, int d_hi,
+                                               const volatile int *u_done, int u_need, BLProf &pf) {
+  const int G = gridDim.x, c = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int m_c = c < p.n ? (p.n - 1 - c) / G + 1 : 0;
+  const int full4 = m_c >> 1;
+  const int last4 = full4 + (m_c & 1);  // float4s holding at least one real source
+  const BLUnits U = bl_units(bt, T, full4);
+  const int nunits = U.ntt * U.nsub;
+  // dirty sub-ranges [sd0, sd1): those meeting [d_lo, d_hi)
+  int sd0 = 0, sd1 = 0;
+  if (d_lo < d_hi) {
+    for (int sb = 0; sb < U.nsub; ++sb) {
+      const int a = (int)(((long long)full4 * sb) / U.nsub);
+      const int e = (sb == U.nsub - 1) ? last4 : (int)(((long long)full4 * (sb + 1)) / U.nsub);
+      if (a < d_hi && d_lo < e) {
+        if (sd1 == 0) sd0 = sb;
+        sd1 = sb + 1;
+      }
+    }
+  }
+  const int nd = sd1 - sd0;
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(unit_ctr, 1);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g >= nunits) break;
+    const int tile = g % U.ntt, rank = g / U.ntt;
+    int sub;
+    if (rank < U.nsub - nd) {
+      sub = rank < sd0 ? rank : rank + nd;
+    } else {
+      sub = sd0 + (rank - (U.nsub - nd));
+      while (*u_done < u_need) __nanosleep(64);  // own update warps not done yet
+    }
+    const int s0 = (int)(((long long)full4 * sub) / U.nsub);
+    const int s1 = (int)(((long long)full4 * (sub + 1)) / U.nsub);
+    float tx[T], ty[T];
+    bl_f2 AX[T], AY[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const int idx = tile * 32 * T + k * 32 + lane;
+      float2 t = make_float2(0.f, 0.f);
+      if (idx < bt) t = tgt ? tgt[idx] : __ldcg(p.xy + lo + idx);
+      tx[k] = t.x;
+      ty[k] = t.y;
+      AX[k] = f2pack(0.f, 0.f);
+      AY[k] = f2pack(0.f, 0.f);
+    }
+    bl_sweep<T, TP>(src4, s0, s1, tx, ty, AX, AY);
+    if ((m_c & 1) && sub == U.nsub - 1) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const int idx = tile * 32 * T + k * 32 + lane;
+      float ax0, ax1, ay0, ay1;
+      f2unpack(AX[k], ax0, ax1);
+      f2unpack(AY[k], ay0, ay1);
+      const float2 r = make_float2(ax0 + ax1, ay0 + ay1);
+      if (idx < bt) {
+        if (U.nsub == 1)
+          part[(size_t)idx * G + c] = r;
+        else
+          red[sub * (U.ntt * 32 * T) + idx] = r;
+      }
+    }
+  }
+  pf.mark(1);
+  __syncthreads();
+  if (U.nsub > 1) {
+    for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
+      float2 acc = red[idx];
+      for (int sb = 1; sb < U.nsub; ++sb) {
+        const float2 v = red[sb * (U.ntt * 32 * T) + idx];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      part[(size_t)idx * G + c] = acc;
+    }
+  }
+}
 
 // ---------------------------------------------------------------- phase R
 template <int T, int TP>
@@ -275,68 +375,9 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
   pf.mark(0);
   __syncthreads();  // targets staged
 
-  // (2) repulsion: units = (target tile of 32·T, sub-range of the CTA's
-  // resident sources), grabbed dynamically by warps (warps that did
-  // attraction items take fewer).  Each unit's result has its own slot and
-  // the slots are combined in a fixed order, so the result does not depend
-  // on which warp ran which unit.
-  // CTA c owns m_c = ceil((n - c)/G) sources: full4 float4s of two real
-  // sources (swept with pairing), then at most one float4 holding one real
-  // source and one far dummy (swept unpaired, by the last sub-range).
-  const int m_c = c < p.n ? (p.n - 1 - c) / G + 1 : 0;
-  const int full4 = m_c >> 1;
-  const BLUnits U = bl_units(bt, T, full4);
-  const int nunits = U.ntt * U.nsub;
-  for (;;) {
-    int u = 0;
-    if (lane == 0) u = atomicAdd(unit_ctr, 1);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= nunits) break;
-    const int tile = u % U.ntt, sub = u / U.ntt;
-    const int s0 = (int)(((long long)full4 * sub) / U.nsub);
-    const int s1 = (int)(((long long)full4 * (sub + 1)) / U.nsub);
-    float tx[T], ty[T];
-    bl_f2 AX[T], AY[T];
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-      const int idx = tile * 32 * T + k * 32 + lane;
-      float2 t = make_float2(0.f, 0.f);
-      if (idx < bt) t = tgt_smem ? tgt[idx] : __ldcg(p.xy + lo + idx);
-      tx[k] = t.x;
-      ty[k] = t.y;
-      AX[k] = f2pack(0.f, 0.f);
-      AY[k] = f2pack(0.f, 0.f);
-    }
-    bl_sweep<T, TP>(src4, s0, s1, tx, ty, AX, AY);
-    if ((m_c & 1) && sub == U.nsub - 1) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-      const int idx = tile * 32 * T + k * 32 + lane;
-      float ax0, ax1, ay0, ay1;
-      f2unpack(AX[k], ax0, ax1);
-      f2unpack(AY[k], ay0, ay1);
-      const float2 r = make_float2(ax0 + ax1, ay0 + ay1);
-      if (idx < bt) {
-        if (U.nsub == 1)
-          p.part[(size_t)idx * G + c] = r;
-        else
-          red[sub * (U.ntt * 32 * T) + idx] = r;
-      }
-    }
-  }
-  pf.mark(1);
-  if (U.nsub > 1) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
-      float2 acc = red[idx];
-      for (int s = 1; s < U.nsub; ++s) {
-        const float2 v = red[s * (U.ntt * 32 * T) + idx];
-        acc.x += v.x;
-        acc.y += v.y;
-      }
-      p.part[(size_t)idx * G + c] = acc;
-    }
-  }
+  // (2) repulsion sweep over the CTA's resident sources
+  bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, 0, 0,
+                        nullptr, 0, pf);
   pf.mark(2);
 }
 
@@ -393,15 +434,209 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
   }
 }
 
+// ------------------------------------------------- pipelined driver (nb >= 4)
+// One grid barrier per batch.  Phase ph runs, in every CTA:
+//   (a) if batch ph-2 closed an iteration: every CTA sums the per-CTA
+//       energies in the same order (identical convergence decision);
+//   (b) commit: owned vertices of batch ph-2 are copied from the owner's
+//       shared copy to xy;
+//   (c) U(ph-1) by "update warps": for each owned vertex v of batch ph-1,
+//       S_v (attraction + neighbour correction, over v's CSR row) and
+//       R_v = Σ_c part[v][c] give f_v; c_v += Step f/||f|| goes to the shared
+//       copy and to pend (NOT to xy, whose batch-(ph-1) entries other CTAs'
+//       update warps may still be reading as frozen coordinates);
+//   (d) cp.async prefetch of batch ph+1's targets into the other tgt buffer;
+//   (e) R(ph): all warps sweep the resident sources against batch ph's
+//       targets; units touching this CTA's just-updated sources run last;
+//   (f) grid barrier.
+// Coordinates seen by batch ph: updated vertices of batch ph-1 live in
+// pend until committed in phase ph+1, so a neighbour j of a batch-ph vertex
+// is read from pend when j is in batch ph-1 and from xy otherwise.  This is
+// exactly the frozen-batch semantics of Alg. 2.
+__device__ __forceinline__ void bl_prefetch_targets(const BLKParams &p, int lo, int bt,
+                                                    float2 *dst) {
+  const int npairs = bt >> 1;
+  for (int i = threadIdx.x; i < npairs; i += BL_NT) {
+    const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst + 2 * i);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(p.xy + lo + 2 * i)
+                 : "memory");
+  }
+  if ((bt & 1) && threadIdx.x == 0) dst[bt - 1] = __ldcg(p.xy + lo + bt - 1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bl_commit(const BLKParams &p, int q, const float4 *src4) {
+  const int G = gridDim.x, c = blockIdx.x;
+  const int lo = (q % p.nb) * p.b, hi = min(lo + p.b, p.n);
+  const int v0 = lo + ((c - lo % G) + G) % G;
+  for (int v = v0 + threadIdx.x * G; v < hi; v += BL_NT * G) p.xy[v] = bl_src_get(src4, (v - c) / G);
+}
+
+// Update of one owned vertex v of batch q (warp-cooperative).
+__device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, double stepd,
+                                              float4 *src4, double &e_acc) {
+  const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
+  const int lo = (q % p.nb) * p.b;
+  const int local = v - lo;
+  // neighbours in batch q-1 are read from pend (committed only next phase)
+  int plo = 0, phi = 0;
+  const float2 *pend_prev = p.pend + (size_t)((q - 1) & 1) * p.b;
+  if (q >= 1) {
+    plo = ((q - 1) % p.nb) * p.b;
+    phi = min(plo + p.b, p.n);
+  }
+  const float2 ci = bl_src_get(src4, (v - c) / G);
+  const float2 *row = p.part + (size_t)(q & 1) * p.b * G + (size_t)local * G;
+  float rx = 0.f, ry = 0.f;
+#pragma unroll 8
+  for (int cc = lane; cc < G; cc += 32) {
+    const float2 t = __ldcg(row + cc);
+    rx += t.x;
+    ry += t.y;
+  }
+  const int k0 = __ldg(p.rowptr + v), k1 = __ldg(p.rowptr + v + 1);
+  const float rep = (p.flags & 1u) ? 0.f : p.ck2;
+  float sx = 0.f, sy = 0.f;
+#pragma unroll 4
+  for (int k = k0 + lane; k < k1; k += 32) {
+    const int j = __ldg(p.colidx + k);
+    const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+    const float dx = cj.x - ci.x, dy = cj.y - ci.y;
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+    const float rs = bl_rsqrt(d2);
+    const float d = d2 * rs;
+    const float coef = fmaf(rep * rs, rs, d * p.invK);
+    sx = fmaf(coef, dx, sx);
+    sy = fmaf(coef, dy, sy);
+  }
+  rx = bl_warp_sum0(rx);
+  ry = bl_warp_sum0(ry);
+  sx = bl_warp_sum0(sx);
+  sy = bl_warp_sum0(sy);
+  if (lane == 0) {
+    const float fx = fmaf(-p.ck2, rx, sx);
+    const float fy = fmaf(-p.ck2, ry, sy);
+    const double qq = (double)fx * fx + (double)fy * fy;
+    float2 cv = ci;
+    if (qq > 0.0) {
+      const double sc = stepd / sqrt(qq);
+      cv.x = (float)((double)cv.x + sc * fx);
+      cv.y = (float)((double)cv.y + sc * fy);
+      bl_src_set(src4, (v - c) / G, cv);
+    }
+    p.pend[(size_t)(q & 1) * p.b + local] = cv;
+    e_acc += qq;
+  }
+}
+
+template <int T, int TP>
+__device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src4, float2 *tgt,
+                                                 float2 *red, int *unit_ctr, int *u_done,
+                                                 double *e_warp, BLProf &pf, unsigned &bar_target) {
+  const int G = gridDim.x, c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = p.nb;
+  const long long ptot = (long long)p.iters * nb;
+  const bool mb_stop = p.max_batches > 0 && p.max_batches < ptot;
+  const int P = mb_stop ? p.max_batches : (int)ptot;
+  double step_u = p.step0;  // Step of the batch being updated
+  double e_acc = 0.0, e_prev = 0.0;
+
+  bl_prefetch_targets(p, 0, min(p.b, p.n), tgt);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+
+  for (int ph = 0; ph <= P + 1; ++ph) {
+    // (a) energy of the iteration closed by batch ph-2
+    const int q2 = ph - 2;
+    if (q2 >= 0 && (q2 % nb == nb - 1 || q2 == P - 1)) {
+      const int it = q2 / nb;
+      double E = 0.0;
+      for (int cc = 0; cc < G; ++cc) E += __ldcg(p.e_cta + (it & 1) * G + cc);
+      if (c == 0 && threadIdx.x == 0) p.energy[it] = E;
+      const bool complete = (q2 % nb == nb - 1);
+      if (complete && q2 < P - 1 && p.tol > 0.0 && it > 0 && fabs(E - e_prev) < p.tol) {
+        bl_commit(p, q2, src4);
+        if (c == 0 && threadIdx.x == 0) *p.iters_done = it + 1;
+        pf.flush(p);
+        return;
+      }
+      e_prev = E;
+    }
+    // (b) commit batch ph-2
+    if (q2 >= 0) bl_commit(p, q2, src4);
+    if (ph == P + 1) break;
+    pf.mark(3);
+    // (c) U(ph-1) by the update warps
+    const int q1 = ph - 1;
+    int u_need = 0, d_lo = 0, d_hi = 0;
+    if (q1 >= 0) {
+      if (q1 > 0 && q1 % nb == 0) step_u = step_u * p.cooling;
+      const int lo1 = (q1 % nb) * p.b, hi1 = min(lo1 + p.b, p.n);
+      const int v0 = lo1 + ((c - lo1 % G) + G) % G;
+      const int owned = v0 < hi1 ? (hi1 - 1 - v0) / G + 1 : 0;
+      u_need = min(owned, BL_NW);
+      if (owned > 0) {
+        const int k_lo = (v0 - c) / G;
+        d_lo = k_lo >> 1;
+        d_hi = ((k_lo + owned - 1) >> 1) + 1;
+      }
+      if (warp < u_need) {
+        for (int i = warp; i < owned; i += BL_NW) bl_update_one(p, q1, v0 + i * G, step_u, src4, e_acc);
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          atomicAdd(u_done, 1);
+        }
+      }
+    }
+    pf.mark(4);
+    // (d) prefetch batch ph+1's targets
+    if (ph + 1 < P) {
+      const int lo_n = ((ph + 1) % nb) * p.b;
+      bl_prefetch_targets(p, lo_n, min(p.b, p.n - lo_n), tgt + ((ph + 1) & 1) * BL_TGT_CAP);
+    }
+    // (e) R(ph)
+    if (ph < P) {
+      const int lo = (ph % nb) * p.b, bt = min(p.b, p.n - lo);
+      bl_sweep_units<T, TP>(p, lo, bt, src4, tgt + (ph & 1) * BL_TGT_CAP, red, unit_ctr,
+                            p.part + (size_t)(ph & 1) * p.b * G, d_lo, d_hi, u_done, u_need, pf);
+    }
+    pf.mark(2);
+    // energy of an iteration closed by batch q1 (after all update warps)
+    if (q1 >= 0 && (q1 % nb == nb - 1 || q1 == P - 1)) {
+      __syncthreads();
+      if (lane == 0) e_warp[warp] = e_acc;
+      e_acc = 0.0;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double e = 0.0;
+        for (int w = 0; w < BL_NW; ++w) e += e_warp[w];
+        p.e_cta[((q1 / nb) & 1) * G + c] = e;
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    bl_grid_sync(p.bar, bar_target, unit_ctr, u_done);
+    pf.mark(5);
+  }
+  if (c == 0 && threadIdx.x == 0) *p.iters_done = mb_stop ? (P - 1) / nb : p.iters;
+  pf.mark(6);
+  pf.flush(p);
+}
+
 template <int T, int TP>
 __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   extern __shared__ float4 bl_smem[];
   float4 *src4 = bl_smem;
   float2 *tgt = reinterpret_cast<float2 *>(bl_smem + p.chunk4);
-  float2 *red = tgt + BL_TGT_CAP;
+  float2 *red = tgt + 2 * BL_TGT_CAP;
   __shared__ double e_warp[BL_NW];
   __shared__ int unit_ctr;
-  if (threadIdx.x == 0) unit_ctr = 0;
+  __shared__ int u_done;
+  if (threadIdx.x == 0) {
+    unit_ctr = 0;
+    u_done = 0;
+  }
 
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -422,6 +657,11 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
     bl_phase_R<T, TP>(p, p.first, p.count, src4, tgt, red, &unit_ctr, pf);
     bl_grid_sync(p.bar, bar_target, &unit_ctr);
     bl_phase_U(p, p.first, p.count, 0.0, src4, e_dummy);
+    return;
+  }
+
+  if (p.pipelined) {
+    bl_run_pipelined<T, TP>(p, src4, tgt, red, &unit_ctr, &u_done, e_warp, pf, bar_target);
     return;
   }
 
