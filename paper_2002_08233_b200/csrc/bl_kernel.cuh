@@ -435,41 +435,77 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
 }
 
 // ------------------------------------------------- pipelined driver (nb >= 4)
-// One grid barrier per batch.  Phase ph runs, in every CTA:
-//   (a) if batch ph-2 closed an iteration: every CTA sums the per-CTA
-//       energies in the same order (identical convergence decision);
-//   (b) commit: owned vertices of batch ph-2 are copied from the owner's
-//       shared copy to xy;
-//   (c) U(ph-1) by "update warps": for each owned vertex v of batch ph-1,
-//       S_v (attraction + neighbour correction, over v's CSR row) and
-//       R_v = Σ_c part[v][c] give f_v; c_v += Step f/||f|| goes to the shared
-//       copy and to pend (NOT to xy, whose batch-(ph-1) entries other CTAs'
-//       update warps may still be reading as frozen coordinates);
-//   (d) cp.async prefetch of batch ph+1's targets into the other tgt buffer;
-//   (e) R(ph): all warps sweep the resident sources against batch ph's
-//       targets; units touching this CTA's just-updated sources run last;
-//   (f) grid barrier.
-// Coordinates seen by batch ph: updated vertices of batch ph-1 live in
-// pend until committed in phase ph+1, so a neighbour j of a batch-ph vertex
-// is read from pend when j is in batch ph-1 and from xy otherwise.  This is
+// One SPLIT grid barrier per batch: a CTA arrives as soon as its partials
+// for batch ph are written and then keeps sweeping; only the warps that need
+// other CTAs' results wait.  Phase ph, in every CTA:
+//   * warp 0 and the update warps wait for barrier ph-1, then
+//       (a) if batch ph-2 closed an iteration: the energy of that iteration
+//           is summed (same order in every CTA -> identical tol decision,
+//           P:1082);
+//       (b) warp 0 commits the CTA's owned vertices of batch ph-2 from its
+//           shared copy to xy and prefetches (cp.async) batch ph+1's targets;
+//       (c) U(ph-1): for each owned vertex v of batch ph-1, S_v (attraction
+//           + neighbour correction over v's CSR row) and R_v = Σ_c part[v][c]
+//           give f_v; c_v += Step f/||f|| goes to the shared copy and to
+//           pend -- NOT to xy, whose batch-(ph-1) entries other CTAs' update
+//           warps may still be reading as frozen coordinates;
+//   * all warps meanwhile sweep batch ph's targets against the resident
+//     sources (R(ph)); units touching sources just updated in (c) run last;
+//   * in-CTA combine -> part[ph&1]; arrive at barrier ph.
+// Coordinates seen by batch ph: the vertices of batch ph-1 live in pend
+// until committed in phase ph+1, so a neighbour j of a batch-ph vertex is
+// read from pend when j is in batch ph-1 and from xy otherwise.  This is
 // exactly the frozen-batch semantics of Alg. 2.
-__device__ __forceinline__ void bl_prefetch_targets(const BLKParams &p, int lo, int bt,
-                                                    float2 *dst) {
+__device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, int *unit_ctr,
+                                               int *u_done) {
+  __syncthreads();
+  target += gridDim.x;  // every thread tracks the barrier target
+  if (threadIdx.x == 0) {
+    *unit_ctr = 0;
+    *u_done = 0;
+    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar)
+                 : "memory");
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void bl_grid_wait_warp(const unsigned *bar, unsigned target) {
+  if ((threadIdx.x & 31) == 0)
+    while ((int)(bl_ld_acquire(bar) - target) < 0) {
+    }
+  __syncwarp();
+}
+
+// cp.async of batch targets [lo, lo+bt) into dst by the calling warp (pairs
+// of targets, 16 bytes each; an odd tail is copied directly).
+__device__ __forceinline__ void bl_prefetch_targets_warp(const BLKParams &p, int lo, int bt,
+                                                         float2 *dst) {
+  const int lane = threadIdx.x & 31;
   const int npairs = bt >> 1;
-  for (int i = threadIdx.x; i < npairs; i += BL_NT) {
+  for (int i = lane; i < npairs; i += 32) {
     const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst + 2 * i);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(p.xy + lo + 2 * i)
                  : "memory");
   }
-  if ((bt & 1) && threadIdx.x == 0) dst[bt - 1] = __ldcg(p.xy + lo + bt - 1);
+  if ((bt & 1) && lane == 0) dst[bt - 1] = __ldcg(p.xy + lo + bt - 1);
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-__device__ __forceinline__ void bl_commit(const BLKParams &p, int q, const float4 *src4) {
-  const int G = gridDim.x, c = blockIdx.x;
+__device__ __forceinline__ void bl_commit_warp(const BLKParams &p, int q, const float4 *src4) {
+  const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b, hi = min(lo + p.b, p.n);
   const int v0 = lo + ((c - lo % G) + G) % G;
-  for (int v = v0 + threadIdx.x * G; v < hi; v += BL_NT * G) p.xy[v] = bl_src_get(src4, (v - c) / G);
+  for (int v = v0 + lane * G; v < hi; v += 32 * G) p.xy[v] = bl_src_get(src4, (v - c) / G);
+}
+
+// Energy of iteration `it` from the per-CTA sums, warp-cooperative, in a
+// fixed order (identical in every CTA).
+__device__ __forceinline__ double bl_energy_sum_warp(const BLKParams &p, int it) {
+  const int G = gridDim.x, lane = threadIdx.x & 31;
+  double e = 0.0;
+  for (int cc = lane; cc < G; cc += 32) e += __ldcg(p.e_cta + (it & 1) * G + cc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  return __shfl_sync(0xffffffffu, e, 0);
 }
 
 // Update of one owned vertex v of batch q (warp-cooperative).
@@ -532,80 +568,106 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
 template <int T, int TP>
 __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src4, float2 *tgt,
                                                  float2 *red, int *unit_ctr, int *u_done,
-                                                 double *e_warp, BLProf &pf, unsigned &bar_target) {
+                                                 int *stop_flag, int *decided, double *e_warp,
+                                                 BLProf &pf, unsigned &bar_target) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = p.nb;
   const long long ptot = (long long)p.iters * nb;
   const bool mb_stop = p.max_batches > 0 && p.max_batches < ptot;
   const int P = mb_stop ? p.max_batches : (int)ptot;
-  double step_u = p.step0;  // Step of the batch being updated
+  double step_u = p.step0;  // Step of the batch being updated (fp64 schedule)
   double e_acc = 0.0, e_prev = 0.0;
+  int done_iters = mb_stop ? (P - 1) / nb : p.iters;
 
-  bl_prefetch_targets(p, 0, min(p.b, p.n), tgt);
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (warp == 0) {
+    bl_prefetch_targets_warp(p, 0, min(p.b, p.n), tgt);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
   __syncthreads();
 
   for (int ph = 0; ph <= P + 1; ++ph) {
-    // (a) energy of the iteration closed by batch ph-2
-    const int q2 = ph - 2;
-    if (q2 >= 0 && (q2 % nb == nb - 1 || q2 == P - 1)) {
-      const int it = q2 / nb;
-      double E = 0.0;
-      for (int cc = 0; cc < G; ++cc) E += __ldcg(p.e_cta + (it & 1) * G + cc);
-      if (c == 0 && threadIdx.x == 0) p.energy[it] = E;
-      const bool complete = (q2 % nb == nb - 1);
-      if (complete && q2 < P - 1 && p.tol > 0.0 && it > 0 && fabs(E - e_prev) < p.tol) {
-        bl_commit(p, q2, src4);
-        if (c == 0 && threadIdx.x == 0) *p.iters_done = it + 1;
-        pf.flush(p);
-        return;
-      }
-      e_prev = E;
-    }
-    // (b) commit batch ph-2
-    if (q2 >= 0) bl_commit(p, q2, src4);
-    if (ph == P + 1) break;
-    pf.mark(3);
-    // (c) U(ph-1) by the update warps
-    const int q1 = ph - 1;
-    int u_need = 0, d_lo = 0, d_hi = 0;
-    if (q1 >= 0) {
-      if (q1 > 0 && q1 % nb == 0) step_u = step_u * p.cooling;
+    const int q2 = ph - 2, q1 = ph - 1;
+    // owned vertices of batch q1 and the float4 range they occupy
+    int owned = 0, v0 = 0, d_lo = 0, d_hi = 0;
+    if (q1 >= 0 && ph <= P) {
       const int lo1 = (q1 % nb) * p.b, hi1 = min(lo1 + p.b, p.n);
-      const int v0 = lo1 + ((c - lo1 % G) + G) % G;
-      const int owned = v0 < hi1 ? (hi1 - 1 - v0) / G + 1 : 0;
-      u_need = min(owned, BL_NW);
+      v0 = lo1 + ((c - lo1 % G) + G) % G;
+      owned = v0 < hi1 ? (hi1 - 1 - v0) / G + 1 : 0;
       if (owned > 0) {
         const int k_lo = (v0 - c) / G;
         d_lo = k_lo >> 1;
         d_hi = ((k_lo + owned - 1) >> 1) + 1;
       }
-      if (warp < u_need) {
-        for (int i = warp; i < owned; i += BL_NW) bl_update_one(p, q1, v0 + i * G, step_u, src4, e_acc);
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          atomicAdd(u_done, 1);
+    }
+    const int u_need = min(owned, BL_NW);
+    if (q1 > 0 && q1 % nb == 0 && ph <= P) step_u = step_u * p.cooling;
+    pf.mark(3);
+    if (warp == 0) {
+      // the CTA's control warp: the only waiter on the grid barrier
+      bool stop = false;
+      if (ph > 0) {
+        bl_grid_wait_warp(p.bar, bar_target);
+        // (a) energy of the iteration closed by batch q2
+        if (q2 >= 0 && (q2 % nb == nb - 1 || q2 == P - 1)) {
+          const int it = q2 / nb;
+          const double E = bl_energy_sum_warp(p, it);
+          if (c == 0 && lane == 0) p.energy[it] = E;
+          if (q2 % nb == nb - 1 && q2 < P - 1 && p.tol > 0.0 && it > 0 &&
+              fabs(E - e_prev) < p.tol) {
+            stop = true;
+            done_iters = it + 1;
+          }
+          e_prev = E;
         }
+        // (b) commit batch q2
+        if (q2 >= 0) bl_commit_warp(p, q2, src4);
+      }
+      if (!stop && ph + 1 < P) {
+        const int lo_n = ((ph + 1) % nb) * p.b;
+        bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), tgt + ((ph + 1) & 1) * BL_TGT_CAP);
+      }
+      if (lane == 0) {
+        if (stop) *(volatile int *)stop_flag = 1;
+        __threadfence_block();
+        *(volatile int *)decided = ph;
+      }
+      __syncwarp();
+    }
+    // (c) U(ph-1) by the update warps, after the control warp's decision
+    if (warp < u_need) {
+      if (warp != 0) {
+        if (lane == 0) {
+          while (*(volatile int *)decided < ph) __nanosleep(32);
+          __threadfence_block();
+        }
+        __syncwarp();
+      }
+      if (!*(volatile int *)stop_flag)
+        for (int i = warp; i < owned; i += BL_NW) bl_update_one(p, q1, v0 + i * G, step_u, src4, e_acc);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(u_done, 1);
       }
     }
     pf.mark(4);
-    // (d) prefetch batch ph+1's targets
-    if (ph + 1 < P) {
-      const int lo_n = ((ph + 1) % nb) * p.b;
-      bl_prefetch_targets(p, lo_n, min(p.b, p.n - lo_n), tgt + ((ph + 1) & 1) * BL_TGT_CAP);
-    }
-    // (e) R(ph)
+    // (d) R(ph): every warp sweeps; dirty units wait for the update warps
     if (ph < P) {
       const int lo = (ph % nb) * p.b, bt = min(p.b, p.n - lo);
       bl_sweep_units<T, TP>(p, lo, bt, src4, tgt + (ph & 1) * BL_TGT_CAP, red, unit_ctr,
                             p.part + (size_t)(ph & 1) * p.b * G, d_lo, d_hi, u_done, u_need, pf);
+    } else {
+      __syncthreads();
     }
     pf.mark(2);
-    // energy of an iteration closed by batch q1 (after all update warps)
-    if (q1 >= 0 && (q1 % nb == nb - 1 || q1 == P - 1)) {
-      __syncthreads();
+    if (*(volatile int *)stop_flag) {
+      if (c == 0 && threadIdx.x == 0) *p.iters_done = done_iters;
+      pf.flush(p);
+      return;
+    }
+    // energy of an iteration closed by batch q1 (all update warps are done)
+    if (q1 >= 0 && ph <= P && (q1 % nb == nb - 1 || q1 == P - 1)) {
       if (lane == 0) e_warp[warp] = e_acc;
       e_acc = 0.0;
       __syncthreads();
@@ -615,11 +677,11 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
         p.e_cta[((q1 / nb) & 1) * G + c] = e;
       }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    bl_grid_sync(p.bar, bar_target, unit_ctr, u_done);
+    if (warp == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+    if (ph <= P) bl_grid_arrive(p.bar, bar_target, unit_ctr, u_done);
     pf.mark(5);
   }
-  if (c == 0 && threadIdx.x == 0) *p.iters_done = mb_stop ? (P - 1) / nb : p.iters;
+  if (c == 0 && threadIdx.x == 0) *p.iters_done = done_iters;
   pf.mark(6);
   pf.flush(p);
 }
@@ -633,9 +695,13 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   __shared__ double e_warp[BL_NW];
   __shared__ int unit_ctr;
   __shared__ int u_done;
+  __shared__ int stop_flag;
+  __shared__ int decided;
   if (threadIdx.x == 0) {
     unit_ctr = 0;
     u_done = 0;
+    stop_flag = 0;
+    decided = -1;
   }
 
   const int G = gridDim.x, c = blockIdx.x;
@@ -661,7 +727,8 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   }
 
   if (p.pipelined) {
-    bl_run_pipelined<T, TP>(p, src4, tgt, red, &unit_ctr, &u_done, e_warp, pf, bar_target);
+    bl_run_pipelined<T, TP>(p, src4, tgt, red, &unit_ctr, &u_done, &stop_flag, &decided, e_warp,
+                            pf, bar_target);
     return;
   }
 

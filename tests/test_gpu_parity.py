@@ -317,3 +317,26 @@ def test_exactly_one_kernel_launch_per_call():
         lay.layout_device(d, iters=5, batch=16)
         torch.cuda.synchronize()
         assert bl.bl_last_launch_count(lay.h) == 1
+
+
+@pytest.mark.parametrize("name", ["C1", "C3b256"])
+def test_pipelined_and_two_barrier_drivers_agree(name, monkeypatch):
+    """The one-barrier pipelined driver (nb >= 4) and the two-barrier driver
+    compute the same method; they differ only in summation order."""
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=2)
+    a, ea, _ = gpu_layout(g, xy0, **p)
+    monkeypatch.setenv("BL_PIPELINE", "0")
+    b, eb, _ = gpu_layout(g, xy0, **p)
+    assert_positions_close(a, b, what="pipelined vs two-barrier")
+    np.testing.assert_allclose(ea, eb, rtol=1e-4)
+
+
+def test_pipelined_max_batches_and_tol():
+    """Stops inside the pipelined driver: max_batches mid-iteration and the
+    tol criterion agree with the two-barrier driver."""
+    g, xy0, cfg = build_config("C1")   # nb = 4 -> pipelined
+    got, _, done = gpu_layout(g, xy0, iters=5, batch=256, max_batches=6)
+    ref, _, rdone = _oracle(g, xy0, dict(iters=5, batch=256, max_batches=6))
+    assert done == rdone == 1
+    assert_positions_close(got, ref, what="pipelined max_batches")
