@@ -123,7 +123,10 @@ extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t 
   return m;
 }
 
-static size_t smem_bytes(int chunk4, int T) { return bl_smem_bytes(chunk4, T); }
+static size_t smem_bytes(int chunk4, int T) {
+  (void)T;
+  return bl_smem_bytes(chunk4);
+}
 
 static int chunk4_for(int n, int G) {
   const int per = (n + G - 1) / G;  // owned sources per CTA (max)
@@ -158,7 +161,7 @@ extern "C" int32_t bl_max_vertices(void) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return 0;
-  const long long room = (long long)optin - 2048 - (long long)bl_smem_bytes(0, 8);
+  const long long room = (long long)optin - 2048 - (long long)bl_smem_bytes(0);
   const long long per = room / (long long)sizeof(float4) * 2;
   const long long n = per * sms;
   return (int32_t)std::min<long long>(n, 0x7fffffff);
@@ -362,7 +365,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // one barrier per batch needs >= 4 batches per iteration,
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
-  k.pipelined = !forces_mode && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 && (((uintptr_t)d_xy) & 15) == 0 &&
+  k.pipelined = !forces_mode && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
+                BL_RED_CAP / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
                 env_int("BL_PIPELINE", 1) != 0;
   k.attr = h->d_attr;
   k.e_cta = h->d_e_cta;

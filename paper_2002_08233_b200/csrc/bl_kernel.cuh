@@ -36,27 +36,42 @@
 #define BL_NW (BL_NT / 32)
 #define BL_ECH 128         // CSR entries per attraction item
 #define BL_EPS2 1e-20f     // self/coincident-pair guard folded into d^2
-#define BL_UNITS (2 * BL_NW)  // target repulsion work units per CTA per batch
-#define BL_TGT_CAP 4096       // batch targets staged in shared memory (else read from L2)
-#define BL_MIN_UNIT4 16       // minimum float4 (2 sources) per repulsion unit
+#define BL_TGT_CAP 2048       // batch targets staged in shared memory (else read from L2)
+#define BL_RED_CAP 8192       // float2 slots for per-(sub-range, target) repulsion partials
+#define BL_MIN_UNIT4 16       // minimum float4 (2 sources) per repulsion sub-range
+#define BL_NSUB_MAX 32
 
 // Partition of one batch's repulsion work inside a CTA: ntt target tiles of
-// 32·T targets x nsub sub-ranges of the CTA's resident sources.
+// 32·T targets x nsub sub-ranges of the CTA's resident sources.  The clean
+// sources are cut into nc sub-ranges of decreasing size ("guided", so that
+// warps that start late -- update warps -- balance out on small units), and
+// the sources this CTA is updating in the same phase (dirty) form the last
+// sub-range.
 struct BLUnits {
-  int ntt, nsub;
+  int ntt, nc, nsub;
 };
-__host__ __device__ inline BLUnits bl_units(int bt, int T, int full4) {
+__host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty) {
   BLUnits u;
   u.ntt = (bt + 32 * T - 1) / (32 * T);
-  int ns = u.ntt >= BL_UNITS ? 1 : BL_UNITS / u.ntt;
-  const int cap = full4 / BL_MIN_UNIT4;
-  if (ns > cap) ns = cap;
-  u.nsub = ns < 1 ? 1 : ns;
+  int cap = BL_RED_CAP / (u.ntt * 32 * T);
+  if (cap > BL_NSUB_MAX) cap = BL_NSUB_MAX;
+  int nc = clean4 / BL_MIN_UNIT4;
+  if (nc > cap - (dirty ? 1 : 0)) nc = cap - (dirty ? 1 : 0);
+  u.nc = nc < 1 ? 1 : nc;
+  u.nsub = u.nc + (dirty ? 1 : 0);
+  if (cap < 1) u.nsub = u.nc = 1;  // very large batches: red unused (nsub == 1)
   return u;
 }
-// shared memory: [src4: chunk4 float4][tgt: 2 x BL_TGT_CAP float2][red: BL_UNITS·32·T float2]
-__host__ __device__ inline size_t bl_smem_bytes(int chunk4, int T) {
-  return (size_t)chunk4 * 16 + (size_t)2 * BL_TGT_CAP * 8 + (size_t)BL_UNITS * 32 * T * 8;
+// start (in the concatenated clean domain of length L) of clean sub-range k
+// of nc, weights nc, nc-1, ..., 1
+__device__ __forceinline__ int bl_guided_start(int k, int nc, int L) {
+  const long long W = (long long)nc * (nc + 1) / 2;
+  const long long cum = (long long)k * nc - (long long)k * (k - 1) / 2;
+  return (int)((L * cum) / W);
+}
+// shared memory: [src4: chunk4 float4][tgt: 2 x BL_TGT_CAP float2][red: BL_RED_CAP float2]
+__host__ __device__ inline size_t bl_smem_bytes(int chunk4) {
+  return (size_t)chunk4 * 16 + (size_t)2 * BL_TGT_CAP * 8 + (size_t)BL_RED_CAP * 8;
 }
 
 struct BLKParams {
@@ -236,17 +251,27 @@ struct BLProf {
   }
 };
 
+// Sweep resident float4 slots [s0, s1) for T targets: paired reciprocals on
+// float4s of two real sources; the (at most one) float4 at index full4 that
+// holds a real source and a far dummy is swept unpaired.
+template <int T, int TP>
+__device__ __forceinline__ void bl_sweep_range(const float4 *src4, int s0, int s1, int full4,
+                                               const float (&tx)[T], const float (&ty)[T],
+                                               bl_f2 (&AX)[T], bl_f2 (&AY)[T]) {
+  const int e = s1 < full4 ? s1 : full4;
+  if (s0 < e) bl_sweep<T, TP>(src4, s0, e, tx, ty, AX, AY);
+  if (s1 > full4 && s0 <= full4) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
+}
+
 // The repulsion work of one batch inside a CTA, as dynamically grabbed
 // units = (target tile of 32·T, sub-range of the CTA's resident sources).
-// Warps that did other work first (attraction items, updates) take fewer
-// units.  Each unit's result has its own slot and the slots are combined in
-// a fixed order, so the result does not depend on which warp ran which unit.
-// CTA c owns m_c = ceil((n - c)/G) sources: full4 float4s of two real
-// sources (swept with pairing), then at most one float4 holding one real
-// source and one far dummy (swept unpaired, by the last sub-range).
-// Units whose source range meets the float4 range [d_lo, d_hi) ("dirty":
-// being updated by this CTA's own update warps in the same phase) are
-// grabbed last and wait until *u_done reaches u_need.
+// Warps that did other work first (updates) take fewer units.  Each unit's
+// result has its own slot and the slots are combined in a fixed order, so
+// the result does not depend on which warp ran which unit.
+// CTA c owns m_c = ceil((n - c)/G) sources in ceil(m_c/2) float4 slots.
+// The slots [d_lo, d_hi) ("dirty": being updated by this CTA's own update
+// warps in the same phase) form the last sub-range, whose units wait until
+// *u_done reaches u_need.
 // tgt: staged targets in shared memory, or nullptr to read them from L2.
 template <int T, int TP>
 __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int bt,
@@ -257,37 +282,19 @@ __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int b
   const int lane = threadIdx.x & 31;
   const int m_c = c < p.n ? (p.n - 1 - c) / G + 1 : 0;
   const int full4 = m_c >> 1;
-  const int last4 = full4 + (m_c & 1);  // float4s holding at least one real source
-  const BLUnits U = bl_units(bt, T, full4);
+  const int last4 = full4 + (m_c & 1);
+  if (d_hi > last4) d_hi = last4;
+  if (d_lo > d_hi) d_lo = d_hi;
+  const bool dirty = d_lo < d_hi;
+  const int clean4 = last4 - (d_hi - d_lo);
+  const BLUnits U = bl_units(bt, T, clean4, dirty);
   const int nunits = U.ntt * U.nsub;
-  // dirty sub-ranges [sd0, sd1): those meeting [d_lo, d_hi)
-  int sd0 = 0, sd1 = 0;
-  if (d_lo < d_hi) {
-    for (int sb = 0; sb < U.nsub; ++sb) {
-      const int a = (int)(((long long)full4 * sb) / U.nsub);
-      const int e = (sb == U.nsub - 1) ? last4 : (int)(((long long)full4 * (sb + 1)) / U.nsub);
-      if (a < d_hi && d_lo < e) {
-        if (sd1 == 0) sd0 = sb;
-        sd1 = sb + 1;
-      }
-    }
-  }
-  const int nd = sd1 - sd0;
   for (;;) {
     int g = 0;
     if (lane == 0) g = atomicAdd(unit_ctr, 1);
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g >= nunits) break;
-    const int tile = g % U.ntt, rank = g / U.ntt;
-    int sub;
-    if (rank < U.nsub - nd) {
-      sub = rank < sd0 ? rank : rank + nd;
-    } else {
-      sub = sd0 + (rank - (U.nsub - nd));
-      while (*u_done < u_need) __nanosleep(64);  // own update warps not done yet
-    }
-    const int s0 = (int)(((long long)full4 * sub) / U.nsub);
-    const int s1 = (int)(((long long)full4 * (sub + 1)) / U.nsub);
+    const int tile = g % U.ntt, sub = g / U.ntt;
     float tx[T], ty[T];
     bl_f2 AX[T], AY[T];
 #pragma unroll
@@ -300,8 +307,18 @@ __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int b
       AX[k] = f2pack(0.f, 0.f);
       AY[k] = f2pack(0.f, 0.f);
     }
-    bl_sweep<T, TP>(src4, s0, s1, tx, ty, AX, AY);
-    if ((m_c & 1) && sub == U.nsub - 1) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
+    if (sub < U.nc) {
+      // clean sub-range: [a, e) of the clean domain [0, d_lo) ++ [d_hi, last4)
+      const int a = bl_guided_start(sub, U.nc, clean4);
+      const int e = bl_guided_start(sub + 1, U.nc, clean4);
+      if (a < d_lo) bl_sweep_range<T, TP>(src4, a, min(e, d_lo), full4, tx, ty, AX, AY);
+      if (e > d_lo)
+        bl_sweep_range<T, TP>(src4, max(a, d_lo) + (d_hi - d_lo), e + (d_hi - d_lo), full4, tx, ty,
+                              AX, AY);
+    } else {
+      while (*u_done < u_need) __nanosleep(64);  // own update warps not done yet
+      bl_sweep_range<T, TP>(src4, d_lo, d_hi, full4, tx, ty, AX, AY);
+    }
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       const int idx = tile * 32 * T + k * 32 + lane;
