@@ -274,7 +274,8 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         "roofline": {
             "bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT,
             "frac": achieved / peak, "traffic": None,
-            "kernel": "bl_layout_kernel<4> (persistent, cooperative)",
+            "kernel": f"bl_layout_kernel<{os.environ.get('BL_T', '8')},{os.environ.get('BL_TP', '3')}>"
+                      " (persistent, cooperative; T targets/thread, TP paired-reciprocal)",
             "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU.RCP/clk x {sm_max:.0f} MHz "
                           f"(sm_max_mhz, {peak_src}); 1 MUFU per pair",
             "frac_at_median_clock": (achieved / (nsm * MUFU_PER_CLK_SM * clocks["sm_mhz"] * 1e6)

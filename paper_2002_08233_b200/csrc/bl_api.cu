@@ -19,10 +19,10 @@
 #include "bl_kernel.cuh"
 
 #ifndef BL_DEFAULT_T
-#define BL_DEFAULT_T 4
+#define BL_DEFAULT_T 8
 #endif
 #ifndef BL_DEFAULT_TP
-#define BL_DEFAULT_TP 0
+#define BL_DEFAULT_TP 3
 #endif
 
 struct bl_ctx {
@@ -123,9 +123,14 @@ extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t 
   return m;
 }
 
-static size_t smem_bytes(int chunk4, int T) {
-  (void)T;
-  return bl_smem_bytes(chunk4);
+static int red_cap_for(int chunk4) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const long long room = (long long)optin - 1024 - (long long)bl_smem_bytes(chunk4, 0);
+  long long cap = room / 8;
+  if (cap > BL_RED_MAX) cap = BL_RED_MAX;
+  return (int)cap;
 }
 
 static int chunk4_for(int n, int G) {
@@ -161,7 +166,7 @@ extern "C" int32_t bl_max_vertices(void) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return 0;
-  const long long room = (long long)optin - 2048 - (long long)bl_smem_bytes(0);
+  const long long room = (long long)optin - 2048 - (long long)bl_smem_bytes(0, BL_RED_MIN);
   const long long per = room / (long long)sizeof(float4) * 2;
   const long long n = per * sms;
   return (int32_t)std::min<long long>(n, 0x7fffffff);
@@ -366,7 +371,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
   k.pipelined = !forces_mode && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
-                BL_RED_CAP / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
+                red_cap_for(chunk4_for(n, G)) / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
                 env_int("BL_PIPELINE", 1) != 0;
   k.attr = h->d_attr;
   k.e_cta = h->d_e_cta;
@@ -376,7 +381,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.f_out = f_out;
   k.prof = h->d_prof;
 
-  const size_t smem = smem_bytes(k.chunk4, h->T);
+  k.red_cap = red_cap_for(k.chunk4);
+  const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   void *kfn = find_variant(h->T, h->TP)->fn;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));

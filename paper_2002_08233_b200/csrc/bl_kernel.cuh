@@ -37,7 +37,8 @@
 #define BL_ECH 128         // CSR entries per attraction item
 #define BL_EPS2 1e-20f     // self/coincident-pair guard folded into d^2
 #define BL_TGT_CAP 2048       // batch targets staged in shared memory (else read from L2)
-#define BL_RED_CAP 8192       // float2 slots for per-(sub-range, target) repulsion partials
+#define BL_RED_MAX 16384      // max float2 slots for per-(sub-range, target) repulsion partials
+#define BL_RED_MIN 4096       // min (the host sizes red from the shared memory left)
 #define BL_MIN_UNIT4 16       // minimum float4 (2 sources) per repulsion sub-range
 #define BL_NSUB_MAX 32
 
@@ -50,10 +51,10 @@
 struct BLUnits {
   int ntt, nc, nsub;
 };
-__host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty) {
+__host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty, int red_cap) {
   BLUnits u;
   u.ntt = (bt + 32 * T - 1) / (32 * T);
-  int cap = BL_RED_CAP / (u.ntt * 32 * T);
+  int cap = red_cap / (u.ntt * 32 * T);
   if (cap > BL_NSUB_MAX) cap = BL_NSUB_MAX;
   int nc = clean4 / BL_MIN_UNIT4;
   if (nc > cap - (dirty ? 1 : 0)) nc = cap - (dirty ? 1 : 0);
@@ -69,9 +70,9 @@ __device__ __forceinline__ int bl_guided_start(int k, int nc, int L) {
   const long long cum = (long long)k * nc - (long long)k * (k - 1) / 2;
   return (int)((L * cum) / W);
 }
-// shared memory: [src4: chunk4 float4][tgt: 2 x BL_TGT_CAP float2][red: BL_RED_CAP float2]
-__host__ __device__ inline size_t bl_smem_bytes(int chunk4) {
-  return (size_t)chunk4 * 16 + (size_t)2 * BL_TGT_CAP * 8 + (size_t)BL_RED_CAP * 8;
+// shared memory: [src4: chunk4 float4][tgt: 2 x BL_TGT_CAP float2][red: red_cap float2]
+__host__ __device__ inline size_t bl_smem_bytes(int chunk4, int red_cap) {
+  return (size_t)chunk4 * 16 + (size_t)2 * BL_TGT_CAP * 8 + (size_t)red_cap * 8;
 }
 
 struct BLKParams {
@@ -80,6 +81,7 @@ struct BLKParams {
   float ck2, invK;
   double step0, cooling, tol;
   int chunk4;            // float4 slots (2 sources each) per CTA chunk
+  int red_cap;           // float2 slots of the shared partial buffer
   int forces_mode, first, count;
   float2 *xy;
   const int *rowptr, *colidx;
@@ -287,7 +289,7 @@ __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int b
   if (d_lo > d_hi) d_lo = d_hi;
   const bool dirty = d_lo < d_hi;
   const int clean4 = last4 - (d_hi - d_lo);
-  const BLUnits U = bl_units(bt, T, clean4, dirty);
+  const BLUnits U = bl_units(bt, T, clean4, dirty, p.red_cap);
   const int nunits = U.ntt * U.nsub;
   for (;;) {
     int g = 0;

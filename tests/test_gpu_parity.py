@@ -322,9 +322,11 @@ def test_exactly_one_kernel_launch_per_call():
 @pytest.mark.parametrize("name", ["C1", "C3b256"])
 def test_pipelined_and_two_barrier_drivers_agree(name, monkeypatch):
     """The one-barrier pipelined driver (nb >= 4) and the two-barrier driver
-    compute the same method; they differ only in summation order."""
+    compute the same method; they differ only in summation order.  One
+    iteration: at C3 the oracle's own fp32-vs-fp64 spread is already 0.35 x
+    extent after two (chaos)."""
     g, xy0, cfg = build_config(name)
-    p = _params(cfg, iters=2)
+    p = _params(cfg, iters=1)
     a, ea, _ = gpu_layout(g, xy0, **p)
     monkeypatch.setenv("BL_PIPELINE", "0")
     b, eb, _ = gpu_layout(g, xy0, **p)
