@@ -371,6 +371,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
   k.pipelined = !forces_mode && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
+                (b + G - 1) / G <= BL_ETASK_MAX &&
                 red_cap_for(chunk4_for(n, G)) / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
                 env_int("BL_PIPELINE", 1) != 0;
   k.attr = h->d_attr;

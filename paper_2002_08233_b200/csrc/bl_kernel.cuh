@@ -265,90 +265,121 @@ __device__ __forceinline__ void bl_sweep_range(const float4 *src4, int s0, int s
   if (s1 > full4 && s0 <= full4) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
 }
 
-// The repulsion work of one batch inside a CTA, as dynamically grabbed
-// units = (target tile of 32·T, sub-range of the CTA's resident sources).
-// Warps that did other work first (updates) take fewer units.  Each unit's
-// result has its own slot and the slots are combined in a fixed order, so
-// the result does not depend on which warp ran which unit.
-// CTA c owns m_c = ceil((n - c)/G) sources in ceil(m_c/2) float4 slots.
-// The slots [d_lo, d_hi) ("dirty": being updated by this CTA's own update
-// warps in the same phase) form the last sub-range, whose units wait until
-// *u_done reaches u_need.
+// Geometry of CTA c's resident sources: m_c = ceil((n - c)/G) owned
+// sources in float4 slots [0, last4); slots [0, full4) hold two real
+// sources, slot full4 (if m_c is odd) one real source and a far dummy.
+// [d_lo, d_hi): slots holding the `owned` sources k_lo.. being updated by
+// this CTA in the current phase ("dirty"); clean4 = slots outside them.
+struct BLGeom {
+  int full4, last4, d_lo, d_hi, clean4;
+};
+__device__ __forceinline__ BLGeom bl_geom(int c, int G, int n, int k_lo, int owned) {
+  BLGeom g;
+  const int m_c = c < n ? (n - 1 - c) / G + 1 : 0;
+  g.full4 = m_c >> 1;
+  g.last4 = g.full4 + (m_c & 1);
+  g.d_lo = g.d_hi = 0;
+  if (owned > 0) {
+    g.d_lo = k_lo >> 1;
+    g.d_hi = ((k_lo + owned - 1) >> 1) + 1;
+    if (g.d_hi > g.last4) g.d_hi = g.last4;
+    if (g.d_lo > g.d_hi) g.d_lo = g.d_hi;
+  }
+  g.clean4 = g.last4 - (g.d_hi - g.d_lo);
+  return g;
+}
+
+// One repulsion work unit g = (target tile g % ntt, sub-range g / ntt):
+// clean sub-ranges are guided cuts of [0, d_lo) ++ [d_hi, last4); the last
+// sub-range (if any) is the dirty slots.  The result goes to its own slot
+// (red, or part directly when there is a single sub-range).
 // tgt: staged targets in shared memory, or nullptr to read them from L2.
+template <int T, int TP>
+__device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, const float4 *src4,
+                                           const float2 *tgt, float2 *red, float2 *part, int g,
+                                           const BLUnits &U, const BLGeom &geo) {
+  const int G = gridDim.x, c = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int tile = g % U.ntt, sub = g / U.ntt;
+  float tx[T], ty[T];
+  bl_f2 AX[T], AY[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const int idx = tile * 32 * T + k * 32 + lane;
+    float2 t = make_float2(0.f, 0.f);
+    if (idx < bt) t = tgt ? tgt[idx] : __ldcg(p.xy + lo + idx);
+    tx[k] = t.x;
+    ty[k] = t.y;
+    AX[k] = f2pack(0.f, 0.f);
+    AY[k] = f2pack(0.f, 0.f);
+  }
+  const int dw = geo.d_hi - geo.d_lo;
+  if (sub < U.nc) {
+    const int a = bl_guided_start(sub, U.nc, geo.clean4);
+    const int e = bl_guided_start(sub + 1, U.nc, geo.clean4);
+    if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY);
+    if (e > geo.d_lo)
+      bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY);
+  } else {
+    bl_sweep_range<T, TP>(src4, geo.d_lo, geo.d_hi, geo.full4, tx, ty, AX, AY);
+  }
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    const int idx = tile * 32 * T + k * 32 + lane;
+    float ax0, ax1, ay0, ay1;
+    f2unpack(AX[k], ax0, ax1);
+    f2unpack(AY[k], ay0, ay1);
+    const float2 r = make_float2(ax0 + ax1, ay0 + ay1);
+    if (idx < bt) {
+      if (U.nsub == 1)
+        part[(size_t)idx * G + c] = r;
+      else
+        red[sub * (U.ntt * 32 * T) + idx] = r;
+    }
+  }
+}
+
+// Fixed-order combine of the sub-range slots into part[target][c] (after a
+// CTA barrier).
+template <int T>
+__device__ __forceinline__ void bl_combine(const BLKParams &p, int bt, const float2 *red,
+                                           float2 *part, const BLUnits &U) {
+  if (U.nsub <= 1) return;
+  const int G = gridDim.x, c = blockIdx.x;
+  for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
+    float2 acc = red[idx];
+    for (int sb = 1; sb < U.nsub; ++sb) {
+      const float2 v = red[sb * (U.ntt * 32 * T) + idx];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    part[(size_t)idx * G + c] = acc;
+  }
+}
+
+// The repulsion work of one batch inside a CTA (two-barrier driver), as
+// dynamically grabbed units: warps that did attraction items first take
+// fewer.  Each unit's result has its own slot and the slots are combined in
+// a fixed order, so the result does not depend on which warp ran which unit.
 template <int T, int TP>
 __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int bt,
                                                const float4 *src4, const float2 *tgt, float2 *red,
-                                               int *unit_ctr, float2 *part, int d_lo, int d_hi,
-                                               const volatile int *u_done, int u_need, BLProf &pf) {
+                                               int *unit_ctr, float2 *part, BLProf &pf) {
   const int G = gridDim.x, c = blockIdx.x;
   const int lane = threadIdx.x & 31;
-  const int m_c = c < p.n ? (p.n - 1 - c) / G + 1 : 0;
-  const int full4 = m_c >> 1;
-  const int last4 = full4 + (m_c & 1);
-  if (d_hi > last4) d_hi = last4;
-  if (d_lo > d_hi) d_lo = d_hi;
-  const bool dirty = d_lo < d_hi;
-  const int clean4 = last4 - (d_hi - d_lo);
-  const BLUnits U = bl_units(bt, T, clean4, dirty, p.red_cap);
+  const BLGeom geo = bl_geom(c, G, p.n, 0, 0);
+  const BLUnits U = bl_units(bt, T, geo.clean4, false, p.red_cap);
   const int nunits = U.ntt * U.nsub;
   for (;;) {
     int g = 0;
     if (lane == 0) g = atomicAdd(unit_ctr, 1);
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g >= nunits) break;
-    const int tile = g % U.ntt, sub = g / U.ntt;
-    float tx[T], ty[T];
-    bl_f2 AX[T], AY[T];
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-      const int idx = tile * 32 * T + k * 32 + lane;
-      float2 t = make_float2(0.f, 0.f);
-      if (idx < bt) t = tgt ? tgt[idx] : __ldcg(p.xy + lo + idx);
-      tx[k] = t.x;
-      ty[k] = t.y;
-      AX[k] = f2pack(0.f, 0.f);
-      AY[k] = f2pack(0.f, 0.f);
-    }
-    if (sub < U.nc) {
-      // clean sub-range: [a, e) of the clean domain [0, d_lo) ++ [d_hi, last4)
-      const int a = bl_guided_start(sub, U.nc, clean4);
-      const int e = bl_guided_start(sub + 1, U.nc, clean4);
-      if (a < d_lo) bl_sweep_range<T, TP>(src4, a, min(e, d_lo), full4, tx, ty, AX, AY);
-      if (e > d_lo)
-        bl_sweep_range<T, TP>(src4, max(a, d_lo) + (d_hi - d_lo), e + (d_hi - d_lo), full4, tx, ty,
-                              AX, AY);
-    } else {
-      while (*u_done < u_need) __nanosleep(64);  // own update warps not done yet
-      bl_sweep_range<T, TP>(src4, d_lo, d_hi, full4, tx, ty, AX, AY);
-    }
-#pragma unroll
-    for (int k = 0; k < T; ++k) {
-      const int idx = tile * 32 * T + k * 32 + lane;
-      float ax0, ax1, ay0, ay1;
-      f2unpack(AX[k], ax0, ax1);
-      f2unpack(AY[k], ay0, ay1);
-      const float2 r = make_float2(ax0 + ax1, ay0 + ay1);
-      if (idx < bt) {
-        if (U.nsub == 1)
-          part[(size_t)idx * G + c] = r;
-        else
-          red[sub * (U.ntt * 32 * T) + idx] = r;
-      }
-    }
+    bl_do_unit<T, TP>(p, lo, bt, src4, tgt, red, part, g, U, geo);
   }
   pf.mark(1);
   __syncthreads();
-  if (U.nsub > 1) {
-    for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
-      float2 acc = red[idx];
-      for (int sb = 1; sb < U.nsub; ++sb) {
-        const float2 v = red[sb * (U.ntt * 32 * T) + idx];
-        acc.x += v.x;
-        acc.y += v.y;
-      }
-      part[(size_t)idx * G + c] = acc;
-    }
-  }
+  bl_combine<T>(p, bt, red, part, U);
 }
 
 // ---------------------------------------------------------------- phase R
@@ -395,8 +426,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
   __syncthreads();  // targets staged
 
   // (2) repulsion sweep over the CTA's resident sources
-  bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, 0, 0,
-                        nullptr, 0, pf);
+  bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, pf);
   pf.mark(2);
 }
 
@@ -454,44 +484,58 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
 }
 
 // ------------------------------------------------- pipelined driver (nb >= 4)
-// One SPLIT grid barrier per batch: a CTA arrives as soon as its partials
-// for batch ph are written and then keeps sweeping; only the warps that need
-// other CTAs' results wait.  Phase ph, in every CTA:
-//   * warp 0 and the update warps wait for barrier ph-1, then
-//       (a) if batch ph-2 closed an iteration: the energy of that iteration
-//           is summed (same order in every CTA -> identical tol decision,
+// One SPLIT grid barrier per batch and a per-CTA task queue.  A CTA arrives
+// at barrier ph as soon as its partials for batch ph are written; the work
+// of phase ph+1 that depends on other CTAs (control, updates) is picked up
+// by whichever warp notices that the barrier has completed, while the
+// other warps keep sweeping -- the barrier latency and the latency-bound
+// updates hide behind the FP32/SFU-bound sweep.  Tasks of phase ph:
+//   control (one warp, once the barrier ph-1 has completed):
+//       (a) if batch ph-2 closed an iteration: that iteration's energy,
+//           summed in the same order in every CTA (identical tol decision,
 //           P:1082);
-//       (b) warp 0 commits the CTA's owned vertices of batch ph-2 from its
-//           shared copy to xy and prefetches (cp.async) batch ph+1's targets;
-//       (c) U(ph-1): for each owned vertex v of batch ph-1, S_v (attraction
-//           + neighbour correction over v's CSR row) and R_v = Σ_c part[v][c]
-//           give f_v; c_v += Step f/||f|| goes to the shared copy and to
-//           pend -- NOT to xy, whose batch-(ph-1) entries other CTAs' update
-//           warps may still be reading as frozen coordinates;
-//   * all warps meanwhile sweep batch ph's targets against the resident
-//     sources (R(ph)); units touching sources just updated in (c) run last;
-//   * in-CTA combine -> part[ph&1]; arrive at barrier ph.
+//       (b) commit: the CTA's owned vertices of batch ph-2 are copied from
+//           its shared copy to xy;
+//       (c) cp.async prefetch of batch ph+1's targets;
+//   update tasks (after control), one per owned vertex v of batch ph-1:
+//       S_v (attraction + neighbour correction over v's CSR row) and
+//       R_v = Σ_c part[v][c] give f_v; c_v += Step f/||f|| goes to the shared
+//       copy and to pend -- NOT to xy, whose batch-(ph-1) entries other CTAs'
+//       update tasks may still be reading as frozen coordinates;
+//   sweep units of R(ph): clean ones any time; the "dirty" sub-range (this
+//       CTA's sources updated in this phase) after the update tasks.
+// Then: in-CTA combine -> part[ph&1]; arrive at barrier ph.
 // Coordinates seen by batch ph: the vertices of batch ph-1 live in pend
 // until committed in phase ph+1, so a neighbour j of a batch-ph vertex is
 // read from pend when j is in batch ph-1 and from xy otherwise.  This is
 // exactly the frozen-batch semantics of Alg. 2.
-__device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, int *unit_ctr,
-                                               int *u_done) {
+#define BL_ETASK_MAX 64  // owned vertices per CTA per batch (b <= 64·G)
+
+struct BLShared {
+  int unit_ctr;   // next sweep unit
+  int u_next;     // next update task
+  int u_done;     // update tasks finished
+  int stop_flag;  // tol convergence reached
+  int ready;      // last phase whose control work is done
+  int ctrl_claim; // last phase whose control work was claimed
+  int done_iters;
+  double e_prev;  // energy of the previous completed iteration
+  double e_acc;   // this CTA's energy of the running iteration
+  double e_task[BL_ETASK_MAX];
+  double e_warp[BL_NW];
+};
+
+__device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, BLShared &sh) {
   __syncthreads();
   target += gridDim.x;  // every thread tracks the barrier target
   if (threadIdx.x == 0) {
-    *unit_ctr = 0;
-    *u_done = 0;
+    sh.unit_ctr = 0;
+    sh.u_next = 0;
+    sh.u_done = 0;
     asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar)
                  : "memory");
   }
   __syncthreads();
-}
-__device__ __forceinline__ void bl_grid_wait_warp(const unsigned *bar, unsigned target) {
-  if ((threadIdx.x & 31) == 0)
-    while ((int)(bl_ld_acquire(bar) - target) < 0) {
-    }
-  __syncwarp();
 }
 
 // cp.async of batch targets [lo, lo+bt) into dst by the calling warp (pairs
@@ -527,9 +571,9 @@ __device__ __forceinline__ double bl_energy_sum_warp(const BLKParams &p, int it)
   return __shfl_sync(0xffffffffu, e, 0);
 }
 
-// Update of one owned vertex v of batch q (warp-cooperative).
+// Update of one owned vertex v of batch q (warp-cooperative); ||f||^2 -> *eq.
 __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, double stepd,
-                                              float4 *src4, double &e_acc) {
+                                              float4 *src4, double *eq) {
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b;
   const int local = v - lo;
@@ -580,127 +624,195 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       bl_src_set(src4, (v - c) / G, cv);
     }
     p.pend[(size_t)(q & 1) * p.b + local] = cv;
-    e_acc += qq;
+    *eq = qq;
+  }
+}
+
+// Phase geometry shared by all warps of a CTA.
+struct BLPhase {
+  int ph, P, q1, q2;
+  int owned, v0;      // owned vertices of batch q1: v0, v0+G, ...
+  double step_u;      // Step of batch q1 (fp64 schedule)
+  float2 *tgt_next;   // staging buffer for batch ph+1's targets
+};
+
+__device__ __forceinline__ bool bl_closes_iteration(int q, int nb, int P) {
+  return q % nb == nb - 1 || q == P - 1;
+}
+
+// Control work of phase ph, attempted by a warp between tasks: if barrier
+// ph-1 has completed and no other warp claimed it, do (a)-(c) and publish.
+__device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase &f,
+                                               const float4 *src4, BLShared &sh,
+                                               unsigned bar_target) {
+  const int lane = threadIdx.x & 31;
+  int go = 0;
+  if (lane == 0 && (int)(bl_ld_acquire(p.bar) - bar_target) >= 0)
+    go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
+  go = __shfl_sync(0xffffffffu, go, 0);
+  if (!go) return;
+  __syncwarp();  // order the lanes' reads after lane 0's acquire
+  bool stop = false;
+  const int nb = p.nb;
+  if (f.q2 >= 0 && bl_closes_iteration(f.q2, nb, f.P)) {
+    const int it = f.q2 / nb;
+    const double E = bl_energy_sum_warp(p, it);
+    if (blockIdx.x == 0 && lane == 0) p.energy[it] = E;
+    if (f.q2 % nb == nb - 1 && f.q2 < f.P - 1 && p.tol > 0.0 && it > 0 &&
+        fabs(E - sh.e_prev) < p.tol) {
+      stop = true;
+      if (lane == 0) sh.done_iters = it + 1;
+    }
+    __syncwarp();
+    if (lane == 0) sh.e_prev = E;
+  }
+  if (f.q2 >= 0) bl_commit_warp(p, f.q2, src4);
+  if (!stop && f.ph + 1 < f.P) {
+    const int lo_n = ((f.ph + 1) % nb) * p.b;
+    bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), f.tgt_next);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (stop) *(volatile int *)&sh.stop_flag = 1;
+    __threadfence_block();
+    *(volatile int *)&sh.ready = f.ph;
+  }
+  __syncwarp();
+}
+
+// Try to take and run one update task; returns true if one was run.
+__device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase &f, float4 *src4,
+                                              BLShared &sh) {
+  const int lane = threadIdx.x & 31;
+  const volatile BLShared &vs = sh;
+  if (vs.ready != f.ph || vs.stop_flag || vs.u_next >= f.owned) return false;
+  int t = f.owned;
+  if (lane == 0) t = atomicAdd(&sh.u_next, 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t >= f.owned) return false;
+  __threadfence_block();  // acquire the control warp's publication
+  bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t]);
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    atomicAdd(&sh.u_done, 1);
+  }
+  return true;
+}
+
+template <int T, int TP>
+__device__ __forceinline__ void bl_phase_tasks(const BLKParams &p, const BLPhase &f,
+                                               float4 *src4, const float2 *tgt, float2 *red,
+                                               BLShared &sh, unsigned bar_target) {
+  const int G = gridDim.x, c = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const volatile BLShared &vs = sh;
+  const bool has_R = f.ph < f.P;
+  const int lo = has_R ? (f.ph % p.nb) * p.b : 0;
+  const int bt = has_R ? min(p.b, p.n - lo) : 0;
+  const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
+  BLUnits U = {1, 0, 0};
+  if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, p.red_cap);
+  const int n_all = has_R ? U.ntt * U.nsub : 0;
+  const int n_clean = has_R ? U.ntt * U.nc : 0;
+  float2 *part = p.part + (size_t)(f.ph & 1) * p.b * G;
+  for (;;) {
+    if (f.ph > 0 && vs.ready != f.ph) bl_try_control(p, f, src4, sh, bar_target);
+    if (bl_try_update(p, f, src4, sh)) continue;
+    int g = n_all;
+    if (vs.unit_ctr < n_all) {
+      if (lane == 0) g = atomicAdd(&sh.unit_ctr, 1);
+      g = __shfl_sync(0xffffffffu, g, 0);
+    }
+    if (g < n_all) {
+      if (g >= n_clean) {
+        // dirty sub-range: needs this CTA's updates of batch q1; help until done
+        for (;;) {
+          if (f.ph > 0 && vs.ready != f.ph) bl_try_control(p, f, src4, sh, bar_target);
+          if (bl_try_update(p, f, src4, sh)) continue;
+          if ((f.ph == 0 || vs.ready == f.ph) && (vs.stop_flag || vs.u_done >= f.owned)) break;
+          __nanosleep(64);
+        }
+        __threadfence_block();
+      }
+      bl_do_unit<T, TP>(p, lo, bt, src4, tgt, red, part, g, U, geo);
+      continue;
+    }
+    // nothing left to grab: done once control ran and every update is taken
+    if ((f.ph == 0 || vs.ready == f.ph) && (vs.stop_flag || vs.u_next >= f.owned)) break;
+    __nanosleep(32);
   }
 }
 
 template <int T, int TP>
 __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src4, float2 *tgt,
-                                                 float2 *red, int *unit_ctr, int *u_done,
-                                                 int *stop_flag, int *decided, double *e_warp,
-                                                 BLProf &pf, unsigned &bar_target) {
+                                                 float2 *red, BLShared &sh, BLProf &pf,
+                                                 unsigned &bar_target) {
   const int G = gridDim.x, c = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = p.nb;
   const long long ptot = (long long)p.iters * nb;
   const bool mb_stop = p.max_batches > 0 && p.max_batches < ptot;
   const int P = mb_stop ? p.max_batches : (int)ptot;
-  double step_u = p.step0;  // Step of the batch being updated (fp64 schedule)
-  double e_acc = 0.0, e_prev = 0.0;
-  int done_iters = mb_stop ? (P - 1) / nb : p.iters;
-
-  if (warp == 0) {
+  double step_u = p.step0;
+  if (threadIdx.x == 0) {
+    sh.done_iters = mb_stop ? (P - 1) / nb : p.iters;
+    sh.e_prev = 0.0;
+    sh.e_acc = 0.0;
+  }
+  if (threadIdx.x < 32) {
     bl_prefetch_targets_warp(p, 0, min(p.b, p.n), tgt);
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (P > 1) bl_prefetch_targets_warp(p, (1 % nb) * p.b, min(p.b, p.n - (1 % nb) * p.b),
+                                        tgt + BL_TGT_CAP);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
   }
   __syncthreads();
 
   for (int ph = 0; ph <= P + 1; ++ph) {
-    const int q2 = ph - 2, q1 = ph - 1;
-    // owned vertices of batch q1 and the float4 range they occupy
-    int owned = 0, v0 = 0, d_lo = 0, d_hi = 0;
-    if (q1 >= 0 && ph <= P) {
-      const int lo1 = (q1 % nb) * p.b, hi1 = min(lo1 + p.b, p.n);
-      v0 = lo1 + ((c - lo1 % G) + G) % G;
-      owned = v0 < hi1 ? (hi1 - 1 - v0) / G + 1 : 0;
-      if (owned > 0) {
-        const int k_lo = (v0 - c) / G;
-        d_lo = k_lo >> 1;
-        d_hi = ((k_lo + owned - 1) >> 1) + 1;
-      }
+    BLPhase f;
+    f.ph = ph;
+    f.P = P;
+    f.q1 = ph - 1;
+    f.q2 = ph - 2;
+    f.owned = 0;
+    f.v0 = 0;
+    if (f.q1 >= 0 && ph <= P) {
+      const int lo1 = (f.q1 % nb) * p.b, hi1 = min(lo1 + p.b, p.n);
+      f.v0 = lo1 + ((c - lo1 % G) + G) % G;
+      f.owned = f.v0 < hi1 ? (hi1 - 1 - f.v0) / G + 1 : 0;
+      if (f.q1 > 0 && f.q1 % nb == 0) step_u = step_u * p.cooling;
     }
-    const int u_need = min(owned, BL_NW);
-    if (q1 > 0 && q1 % nb == 0 && ph <= P) step_u = step_u * p.cooling;
+    f.step_u = step_u;
+    f.tgt_next = tgt + ((ph + 1) & 1) * BL_TGT_CAP;
     pf.mark(3);
-    if (warp == 0) {
-      // the CTA's control warp: the only waiter on the grid barrier
-      bool stop = false;
-      if (ph > 0) {
-        bl_grid_wait_warp(p.bar, bar_target);
-        // (a) energy of the iteration closed by batch q2
-        if (q2 >= 0 && (q2 % nb == nb - 1 || q2 == P - 1)) {
-          const int it = q2 / nb;
-          const double E = bl_energy_sum_warp(p, it);
-          if (c == 0 && lane == 0) p.energy[it] = E;
-          if (q2 % nb == nb - 1 && q2 < P - 1 && p.tol > 0.0 && it > 0 &&
-              fabs(E - e_prev) < p.tol) {
-            stop = true;
-            done_iters = it + 1;
-          }
-          e_prev = E;
-        }
-        // (b) commit batch q2
-        if (q2 >= 0) bl_commit_warp(p, q2, src4);
-      }
-      if (!stop && ph + 1 < P) {
-        const int lo_n = ((ph + 1) % nb) * p.b;
-        bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), tgt + ((ph + 1) & 1) * BL_TGT_CAP);
-      }
-      if (lane == 0) {
-        if (stop) *(volatile int *)stop_flag = 1;
-        __threadfence_block();
-        *(volatile int *)decided = ph;
-      }
-      __syncwarp();
-    }
-    // (c) U(ph-1) by the update warps, after the control warp's decision
-    if (warp < u_need) {
-      if (warp != 0) {
-        if (lane == 0) {
-          while (*(volatile int *)decided < ph) __nanosleep(32);
-          __threadfence_block();
-        }
-        __syncwarp();
-      }
-      if (!*(volatile int *)stop_flag)
-        for (int i = warp; i < owned; i += BL_NW) bl_update_one(p, q1, v0 + i * G, step_u, src4, e_acc);
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        atomicAdd(u_done, 1);
-      }
-    }
-    pf.mark(4);
-    // (d) R(ph): every warp sweeps; dirty units wait for the update warps
-    if (ph < P) {
-      const int lo = (ph % nb) * p.b, bt = min(p.b, p.n - lo);
-      bl_sweep_units<T, TP>(p, lo, bt, src4, tgt + (ph & 1) * BL_TGT_CAP, red, unit_ctr,
-                            p.part + (size_t)(ph & 1) * p.b * G, d_lo, d_hi, u_done, u_need, pf);
-    } else {
-      __syncthreads();
-    }
-    pf.mark(2);
-    if (*(volatile int *)stop_flag) {
-      if (c == 0 && threadIdx.x == 0) *p.iters_done = done_iters;
+    bl_phase_tasks<T, TP>(p, f, src4, tgt + (ph & 1) * BL_TGT_CAP, red, sh, bar_target);
+    pf.mark(1);
+    __syncthreads();
+    if (sh.stop_flag) {
+      if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
       pf.flush(p);
       return;
     }
-    // energy of an iteration closed by batch q1 (all update warps are done)
-    if (q1 >= 0 && ph <= P && (q1 % nb == nb - 1 || q1 == P - 1)) {
-      if (lane == 0) e_warp[warp] = e_acc;
-      e_acc = 0.0;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double e = 0.0;
-        for (int w = 0; w < BL_NW; ++w) e += e_warp[w];
-        p.e_cta[((q1 / nb) & 1) * G + c] = e;
-      }
+    if (ph < P) {
+      const int lo = (ph % nb) * p.b, bt = min(p.b, p.n - lo);
+      const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
+      const BLUnits U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, p.red_cap);
+      bl_combine<T>(p, bt, red, p.part + (size_t)(ph & 1) * p.b * G, U);
     }
-    if (warp == 0) asm volatile("cp.async.wait_all;" ::: "memory");
-    if (ph <= P) bl_grid_arrive(p.bar, bar_target, unit_ctr, u_done);
+    if (threadIdx.x == 0 && f.owned > 0) {
+      double e = sh.e_acc;
+      for (int i = 0; i < f.owned; ++i) e += sh.e_task[i];
+      sh.e_acc = e;
+    }
+    if (f.q1 >= 0 && ph <= P && bl_closes_iteration(f.q1, nb, P) && threadIdx.x == 0) {
+      p.e_cta[((f.q1 / nb) & 1) * G + c] = sh.e_acc;
+      sh.e_acc = 0.0;
+    }
+    pf.mark(2);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (ph <= P) bl_grid_arrive(p.bar, bar_target, sh);
     pf.mark(5);
   }
-  if (c == 0 && threadIdx.x == 0) *p.iters_done = done_iters;
+  if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
   pf.mark(6);
   pf.flush(p);
 }
@@ -711,17 +823,17 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
   float4 *src4 = bl_smem;
   float2 *tgt = reinterpret_cast<float2 *>(bl_smem + p.chunk4);
   float2 *red = tgt + 2 * BL_TGT_CAP;
-  __shared__ double e_warp[BL_NW];
-  __shared__ int unit_ctr;
-  __shared__ int u_done;
-  __shared__ int stop_flag;
-  __shared__ int decided;
+  __shared__ BLShared sh;
   if (threadIdx.x == 0) {
-    unit_ctr = 0;
-    u_done = 0;
-    stop_flag = 0;
-    decided = -1;
+    sh.unit_ctr = 0;
+    sh.u_next = 0;
+    sh.u_done = 0;
+    sh.stop_flag = 0;
+    sh.ready = 0;
+    sh.ctrl_claim = 0;
   }
+  int *unit_ctr = &sh.unit_ctr;
+  double *e_warp = sh.e_warp;
 
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -739,15 +851,14 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
 
   if (p.forces_mode) {
     double e_dummy = 0.0;
-    bl_phase_R<T, TP>(p, p.first, p.count, src4, tgt, red, &unit_ctr, pf);
-    bl_grid_sync(p.bar, bar_target, &unit_ctr);
+    bl_phase_R<T, TP>(p, p.first, p.count, src4, tgt, red, unit_ctr, pf);
+    bl_grid_sync(p.bar, bar_target, unit_ctr);
     bl_phase_U(p, p.first, p.count, 0.0, src4, e_dummy);
     return;
   }
 
   if (p.pipelined) {
-    bl_run_pipelined<T, TP>(p, src4, tgt, red, &unit_ctr, &u_done, &stop_flag, &decided, e_warp,
-                            pf, bar_target);
+    bl_run_pipelined<T, TP>(p, src4, tgt, red, sh, pf, bar_target);
     return;
   }
 
@@ -762,8 +873,8 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b;
       const int bt = min(p.b, p.n - lo);
-      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, &unit_ctr, pf);
-      bl_grid_sync(p.bar, bar_target, &unit_ctr);
+      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, unit_ctr, pf);
+      bl_grid_sync(p.bar, bar_target, unit_ctr);
       pf.mark(3);
       bl_phase_U(p, lo, bt, step, src4, e_acc);
       pf.mark(4);
@@ -779,7 +890,7 @@ __global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
           p.e_cta[(it & 1) * G + c] = e;
         }
       }
-      bl_grid_sync(p.bar, bar_target, &unit_ctr);
+      bl_grid_sync(p.bar, bar_target, unit_ctr);
       pf.mark(5);
       if (last || stop) {
         // every CTA reduces the per-CTA energies in the same order, so the
