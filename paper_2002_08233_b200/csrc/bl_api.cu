@@ -18,6 +18,9 @@
 #include "../../include/bl.h"
 #include "bl_kernel.cuh"
 
+#ifndef BL_DEFAULT_NT
+#define BL_DEFAULT_NT 512
+#endif
 #ifndef BL_DEFAULT_T
 #define BL_DEFAULT_T 8
 #endif
@@ -29,6 +32,7 @@ struct bl_ctx {
   int32_t n = 0, nnz = 0;
   int device = 0, num_sms = 0;
   int G = 0;  // grid size of the persistent kernel
+  int NT = 512; // threads per CTA
   int T = 4;  // register-blocked targets per thread
   int TP = 0; // of which use the paired reciprocal (bl_sweep)
   // device CSR + items
@@ -143,20 +147,23 @@ static int env_int(const char *name, int def) {
   return (s && *s) ? atoi(s) : def;
 }
 
-// Kernel variants (T targets per thread, TP of them paired-reciprocal).
+// Kernel variants (NT threads per CTA, T targets per thread, TP of them
+// paired-reciprocal).  NT x registers is one SM's register file: 512 x 128,
+// 768 x 80, 1024 x 64.
 struct BLVariant {
-  int T, TP;
+  int NT, T, TP;
   void *fn;
 };
-#define BL_V(T, TP) {T, TP, (void *)bl_layout_kernel<T, TP>}
+#define BL_V(NT, T, TP) {NT, T, TP, (void *)bl_layout_kernel<NT, T, TP>}
 static const BLVariant kVariants[] = {
-    BL_V(2, 0), BL_V(2, 1), BL_V(2, 2), BL_V(4, 0), BL_V(4, 1), BL_V(4, 2),
-    BL_V(4, 3), BL_V(4, 4), BL_V(8, 0), BL_V(8, 2), BL_V(8, 3), BL_V(8, 4),
+    BL_V(512, 8, 2),  BL_V(512, 8, 3),  BL_V(512, 8, 4),  BL_V(512, 4, 2),
+    BL_V(768, 6, 2),  BL_V(768, 4, 1),  BL_V(768, 4, 2),
+    BL_V(1024, 4, 1), BL_V(1024, 4, 2), BL_V(1024, 2, 1),
 };
 #undef BL_V
-static const BLVariant *find_variant(int T, int TP) {
+static const BLVariant *find_variant(int NT, int T, int TP) {
   for (const auto &v : kVariants)
-    if (v.T == T && v.TP == TP) return &v;
+    if (v.NT == NT && v.T == T && v.TP == TP) return &v;
   return nullptr;
 }
 
@@ -217,9 +224,11 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   if (cudaGetDevice(&h->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess)
     return bad(fail(h, BL_ECUDA, "no CUDA device"));
+  h->NT = env_int("BL_NT", BL_DEFAULT_NT);
   h->T = env_int("BL_T", BL_DEFAULT_T);
   h->TP = env_int("BL_TP", BL_DEFAULT_TP);
-  if (!find_variant(h->T, h->TP)) {
+  if (!find_variant(h->NT, h->T, h->TP)) {
+    h->NT = BL_DEFAULT_NT;
     h->T = BL_DEFAULT_T;
     h->TP = BL_DEFAULT_TP;
   }
@@ -384,18 +393,19 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
 
   k.red_cap = red_cap_for(k.chunk4);
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
-  void *kfn = find_variant(h->T, h->TP)->fn;
+  const BLVariant *vt = find_variant(h->NT, h->T, h->TP);
+  void *kfn = vt->fn;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
   int occ = 0;
-  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, BL_NT, smem));
+  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, vt->NT, smem));
   if (occ * h->num_sms < G)
     return fail(h, BL_ECUDA, "cooperative grid %d exceeds residency %d x %d SMs", G, occ, h->num_sms);
 
   BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
   void *args[] = {&k};
-  BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(BL_NT), args, smem, st));
+  BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(vt->NT), args, smem, st));
   h->launches = 1;
   return BL_OK;
 }

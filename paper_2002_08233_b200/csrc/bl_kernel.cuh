@@ -13,7 +13,7 @@
 //     * all-pairs repulsion: CTA c holds its owned sources {v : v ≡ c mod G}
 //       resident in shared memory for the whole call; every warp sweeps a
 //       sub-range of them against 32·T register-blocked batch targets,
-//       R_i += Δ_ij / d_ij^2 (branch-free: d^2 = Δx^2 + Δy^2 + 1e-30 makes the
+//       R_i += Δ_ij / d_ij^2 (branch-free: d^2 = Δx^2 + Δy^2 + 2^-63 makes the
 //       self pair and coincident pairs contribute exactly 0, reading C3/C4;
 //       1/d^2 on the SFU via rcp.approx.ftz).  Per-CTA partials go to
 //       part[target][c] after a fixed-order in-CTA combine.
@@ -32,10 +32,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#define BL_NT 512          // threads per CTA (16 warps)
-#define BL_NW (BL_NT / 32)
+// threads per CTA: a template parameter of the kernel (NT, launch bounds);
+// device code reads it as blockDim.x.  BL_NT / BL_NW: the runtime values.
+#define BL_NT ((int)blockDim.x)
+#define BL_NW ((int)(blockDim.x >> 5))
+#define BL_NW_MAX 32
 #define BL_ECH 128         // CSR entries per attraction item
-#define BL_EPS2 1e-20f     // self/coincident-pair guard folded into d^2
+// self/coincident-pair guard folded into d^2: 2^-63, so that
+// eps2*eps2 = 2^-126 is still a normal float and the paired reciprocal
+// 1/(d2a d2b) stays finite even when both pairs are coincident
+#define BL_EPS2 1.0842021724855044e-19f
 #define BL_TGT_CAP 2048       // batch targets staged in shared memory (else read from L2)
 #define BL_RED_MAX 16384      // max float2 slots for per-(sub-range, target) repulsion partials
 #define BL_RED_MIN 4096       // min (the host sizes red from the shared memory left)
@@ -157,7 +163,8 @@ __device__ __forceinline__ float2 bl_src_get(const float4 *src4, int k) {
 //   r = 1/(d2a d2b), INV = (d2b r, d2a r) (FMUL + MUFU + FMUL2), otherwise
 //   two MUFU.RCP.  TP trades SFU work for FP32 work.
 // Requires every D2 lane finite and d2a·d2b a normal float when paired: true
-// for real sources (d^2 >= 1e-20 by the eps fold, < 1e19); dummy (far)
+// for real sources (d^2 >= 2^-63 by the eps fold, so d2a d2b >= 2^-126;
+// d^2 < 1.8e19); dummy (far)
 // sources are only ever swept with TP = 0.
 template <int T, int TP>
 __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0, int s1,
@@ -522,7 +529,7 @@ struct BLShared {
   double e_prev;  // energy of the previous completed iteration
   double e_acc;   // this CTA's energy of the running iteration
   double e_task[BL_ETASK_MAX];
-  double e_warp[BL_NW];
+  double e_warp[BL_NW_MAX];
 };
 
 __device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, BLShared &sh) {
@@ -817,8 +824,8 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
   pf.flush(p);
 }
 
-template <int T, int TP>
-__global__ void __launch_bounds__(BL_NT, 1) bl_layout_kernel(BLKParams p) {
+template <int NT, int T, int TP>
+__global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
   extern __shared__ float4 bl_smem[];
   float4 *src4 = bl_smem;
   float2 *tgt = reinterpret_cast<float2 *>(bl_smem + p.chunk4);

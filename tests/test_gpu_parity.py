@@ -162,6 +162,38 @@ def test_isolated_vertices_and_hubs():
     assert_positions_close(got, ref, what="rmat12")
 
 
+def test_all_vertices_coincident():
+    """Reading C4: coincident pairs contribute nothing, so a layout with every
+    vertex at one point has f = 0 everywhere: no move, zero energy (and no
+    NaN from the paired reciprocal)."""
+    g = grid_graph(20, 30)
+    xy0 = np.full((g.n, 2), 0.375, np.float32)
+    for b in (64, 600):
+        got, tr, done = gpu_layout(g, xy0, iters=2, batch=b)
+        ref, E, _ = _oracle(g, xy0, dict(iters=2, batch=b))
+        assert np.array_equal(ref, xy0) and np.all(E == 0)
+        assert np.array_equal(got, xy0) and done == 2 and np.all(tr == 0)
+
+
+@pytest.mark.parametrize("stride", [1, 148, 296, 37])
+def test_coincident_vertex_pairs(stride):
+    """Duplicated positions (v and v+stride at the same point; 148 = the SM
+    count puts both in one resident float4 of one CTA, so a target sees a
+    coincident pair AND its self pair in one paired reciprocal).  One batch,
+    one iteration vs the oracle (coincident pairs contribute 0, C4)."""
+    g = rmat_graph(11, 8, 0.57, 0.19, 0.19, seed=4)
+    xy0 = uniform_coords(g.n, 11)
+    for v in range(0, g.n - stride, 5):
+        xy0[v + stride] = xy0[v]
+    for p in (dict(iters=1, batch=256, max_batches=1), dict(iters=1, batch=256)):
+        got, tr, _ = gpu_layout(g, xy0, **p)
+        ref, E, _ = _oracle(g, xy0, p)
+        assert np.all(np.isfinite(got))
+        assert_positions_close(got, ref, what=f"coincident stride {stride}")
+        if "max_batches" not in p:
+            assert abs(tr[0] - E[0]) <= 1e-3 * E[0]
+
+
 def test_repulse_neighbors_flag():
     g, xy0 = _small()
     p = dict(iters=1, batch=32, flags=1)
