@@ -51,6 +51,27 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def aggregate_value(units_per_rank: float, world: int, t_max: float) -> float:
+    """Whole-job throughput: the units all ranks processed / the slowest
+    rank's time (replicas: every rank processes the same units)."""
+    return world * units_per_rank / t_max
+
+
+def load_traffic(workload: str, kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed `ncu --set full` capture of this workload's launch
+    (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as fh:
+        d = json.load(fh)
+    e = d.get(workload)
+    if not e or e.get("kernel") != kernel:
+        return None, None
+    return float(e["bytes_per_launch"]), e.get("source")
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -238,7 +259,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     t_local = sum(ms) / 1e3
     t_max = max_over_ranks(t_local, world, dev if world > 1 and args.backend == "nccl" else None)
     pairs_per_step = cfg.iters * g.n * (g.n - 1.0)
-    value = world * args.steps * pairs_per_step / t_max
+    value = aggregate_value(args.steps * pairs_per_step, world, t_max)
     e_last, trace, done = lay.energy(trace_len=cfg.iters)
     assert done == cfg.iters
 
@@ -255,7 +276,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         e_l, _, _ = lay.energy(trace_len=cfg.iters)                # D2H of the energy trace
         tot += time.perf_counter() - t0
     e2e_t = max_over_ranks(tot, world, dev if world > 1 and args.backend == "nccl" else None)
-    e2e_value = world * e2e_steps * pairs_per_step / e2e_t
+    e2e_value = aggregate_value(e2e_steps * pairs_per_step, world, e2e_t)
 
     peaks, peak_src = load_peaks()
     clocks = clk.summary()
@@ -263,6 +284,8 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = nsm * MUFU_PER_CLK_SM * sm_max * 1e6
     achieved = pairs_per_step / (t_local / args.steps)
+    kname = bl.bl_kernel_name(lay.h)
+    traffic, traffic_src = load_traffic(name, kname)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
@@ -273,9 +296,10 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         "iters_per_sec": world * args.steps * cfg.iters / t_max,
         "roofline": {
             "bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT,
-            "frac": achieved / peak, "traffic": None,
-            "kernel": f"bl_layout_kernel<{os.environ.get('BL_T', '8')},{os.environ.get('BL_TP', '3')}>"
-                      " (persistent, cooperative; T targets/thread, TP paired-reciprocal)",
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": traffic_src,
+            "kernel": kname + " (persistent, cooperative; NT threads, T targets/thread, TP of them "
+                              "paired-reciprocal)",
             "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU.RCP/clk x {sm_max:.0f} MHz "
                           f"(sm_max_mhz, {peak_src}); 1 MUFU per pair",
             "frac_at_median_clock": (achieved / (nsm * MUFU_PER_CLK_SM * clocks["sm_mhz"] * 1e6)

@@ -114,6 +114,11 @@ int32_t bl_max_vertices(void);
  * bl_forces call enqueued (the persistent design launches exactly one). */
 int32_t bl_last_launch_count(const bl_ctx *h);
 
+/* Name of the kernel variant h launches, "bl_layout_kernel<NT,T,TP>" (NT
+ * threads per CTA, T register-blocked targets per thread, TP of them with
+ * paired reciprocals).  Static storage owned by h. */
+const char *bl_kernel_name(const bl_ctx *h);
+
 /* Microbenchmark of the roofline denominators on the current device:
  * sustained thread-op rates per SM per clock of (0) 3-register FFMA,
  * (1) MUFU.RCP (rcp.approx.ftz.f32), (2) MUFU.RSQ, (3) packed FFMA2

@@ -59,6 +59,8 @@ def _load() -> ctypes.CDLL:
     lib.bl_max_vertices.restype = i32
     lib.bl_last_launch_count.argtypes = [vp]
     lib.bl_last_launch_count.restype = i32
+    lib.bl_kernel_name.argtypes = [vp]
+    lib.bl_kernel_name.restype = ctypes.c_char_p
     lib.bl_microbench.argtypes = [P(ctypes.c_double)]
     lib.bl_microbench.restype = ctypes.c_int
     lib.bl_debug_profile.argtypes = [vp, vp, i32]
@@ -76,7 +78,7 @@ lib = _load()
 
 # symbols include/bl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bl_params_default", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
-           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_microbench",
+           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_kernel_name", "bl_microbench",
            "bl_debug_profile", "bl_destroy", "bl_status_string", "bl_last_error")
 
 
@@ -160,6 +162,10 @@ def bl_max_vertices() -> int:
 
 def bl_last_launch_count(h: int) -> int:
     return int(lib.bl_last_launch_count(h))
+
+
+def bl_kernel_name(h: int) -> str:
+    return lib.bl_kernel_name(h).decode()
 
 
 def bl_microbench():

@@ -25,7 +25,7 @@
 #define BL_DEFAULT_T 8
 #endif
 #ifndef BL_DEFAULT_TP
-#define BL_DEFAULT_TP 3
+#define BL_DEFAULT_TP 2
 #endif
 
 struct bl_ctx {
@@ -62,6 +62,7 @@ struct bl_ctx {
   bool have_layout = false;
   int32_t launches = 0;
   std::string err;
+  char kname[64] = {0};
 };
 
 static thread_local std::string g_create_err;
@@ -116,6 +117,8 @@ extern "C" const char *bl_last_error(const bl_ctx *h) {
 }
 
 extern "C" int32_t bl_last_launch_count(const bl_ctx *h) { return h ? h->launches : 0; }
+
+extern "C" const char *bl_kernel_name(const bl_ctx *h) { return h ? h->kname : ""; }
 
 // Not part of the public header: phase profile of the last launch when the
 // context was created with BL_PROFILE=1 (debug aid for bench.py --prof).
@@ -232,6 +235,7 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
     h->T = BL_DEFAULT_T;
     h->TP = BL_DEFAULT_TP;
   }
+  snprintf(h->kname, sizeof h->kname, "bl_layout_kernel<%d,%d,%d>", h->NT, h->T, h->TP);
 
   // attraction items: ceil(deg(v)/ECH) per vertex, in vertex order
   h->item_ptr.assign((size_t)n + 1, 0);
@@ -392,6 +396,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.prof = h->d_prof;
 
   k.red_cap = red_cap_for(k.chunk4);
+  k.guided = env_int("BL_GUIDED", 2);
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   const BLVariant *vt = find_variant(h->NT, h->T, h->TP);
   void *kfn = vt->fn;

@@ -70,10 +70,20 @@ __host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirt
   return u;
 }
 // start (in the concatenated clean domain of length L) of clean sub-range k
-// of nc, weights nc, nc-1, ..., 1
-__device__ __forceinline__ int bl_guided_start(int k, int nc, int L) {
-  const long long W = (long long)nc * (nc + 1) / 2;
-  const long long cum = (long long)k * nc - (long long)k * (k - 1) / 2;
+// of nc.  Sizes decrease so that the units grabbed last (the tail of a
+// batch, when warps run out of work) are small:
+//   profile 1: weights nc, nc-1, ..., 1        (linear)
+//   profile 2: weights nc^2, (nc-1)^2, ..., 1  (quadratic; the default)
+__device__ __forceinline__ long long bl_sq_sum(long long m) { return m * (m + 1) * (2 * m + 1) / 6; }
+__device__ __forceinline__ int bl_guided_start(int k, int nc, int L, int profile) {
+  long long W, cum;
+  if (profile == 2) {
+    W = bl_sq_sum(nc);
+    cum = W - bl_sq_sum(nc - k);
+  } else {
+    W = (long long)nc * (nc + 1) / 2;
+    cum = (long long)k * nc - (long long)k * (k - 1) / 2;
+  }
   return (int)((L * cum) / W);
 }
 // shared memory: [src4: chunk4 float4][tgt: 2 x BL_TGT_CAP float2][red: red_cap float2]
@@ -88,6 +98,7 @@ struct BLKParams {
   double step0, cooling, tol;
   int chunk4;            // float4 slots (2 sources each) per CTA chunk
   int red_cap;           // float2 slots of the shared partial buffer
+  int guided;            // sub-range size profile (bl_guided_start)
   int forces_mode, first, count;
   float2 *xy;
   const int *rowptr, *colidx;
@@ -322,8 +333,8 @@ __device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, c
   }
   const int dw = geo.d_hi - geo.d_lo;
   if (sub < U.nc) {
-    const int a = bl_guided_start(sub, U.nc, geo.clean4);
-    const int e = bl_guided_start(sub + 1, U.nc, geo.clean4);
+    const int a = bl_guided_start(sub, U.nc, geo.clean4, p.guided);
+    const int e = bl_guided_start(sub + 1, U.nc, geo.clean4, p.guided);
     if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY);
     if (e > geo.d_lo)
       bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY);
@@ -768,9 +779,13 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
   }
   if (threadIdx.x < 32) {
     bl_prefetch_targets_warp(p, 0, min(p.b, p.n), tgt);
-    if (P > 1) bl_prefetch_targets_warp(p, (1 % nb) * p.b, min(p.b, p.n - (1 % nb) * p.b),
-                                        tgt + BL_TGT_CAP);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    if (P > 1) {
+      bl_prefetch_targets_warp(p, (1 % nb) * p.b, min(p.b, p.n - (1 % nb) * p.b),
+                               tgt + BL_TGT_CAP);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // batch 0's group landed
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");  // only batch 0 was issued
+    }
   }
   __syncthreads();
 

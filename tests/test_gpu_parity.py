@@ -374,3 +374,21 @@ def test_pipelined_max_batches_and_tol():
     ref, _, rdone = _oracle(g, xy0, dict(iters=5, batch=256, max_batches=6))
     assert done == rdone == 1
     assert_positions_close(got, ref, what="pipelined max_batches")
+
+
+@pytest.mark.parametrize("name", ["C1", "C3b1024"])
+def test_one_batch_repeated(name):
+    """Regression: with a single batch to run, the kernel prologue must wait
+    for batch 0's cp.async target prefetch (it used to wait for all but the
+    newest group, i.e. not at all).  Repeated, because the race was timing
+    dependent."""
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=1, max_batches=1)
+    ref, _, _ = _oracle(g, xy0, p)
+    first = None
+    for _ in range(10):
+        got, _, _ = gpu_layout(g, xy0, **p)
+        assert_positions_close(got, ref, what=f"{name} one batch (repeated)")
+        if first is None:
+            first = got
+        assert np.array_equal(got, first)
