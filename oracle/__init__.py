@@ -21,6 +21,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bl_oracle.c")
 _IMPL = os.path.join(_HERE, "bl_oracle_impl.h")
+_BH = os.path.join(_HERE, "bl_oracle_bh.h")
 _SO = os.path.join(_HERE, "libbl_oracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -30,7 +31,7 @@ REPULSE_NEIGHBORS = 1
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc: -O2 -ffp-contract=off, no fast-math."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_IMPL))
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_IMPL), os.path.getmtime(_BH))
     if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= newest:
         return _SO
     tmp = _SO + f".tmp{os.getpid()}"
@@ -60,6 +61,15 @@ def _load():
             f.argtypes = [vp, R, R, R, vp]
             f.restype = ctypes.c_int
         lib.oracle_max_threads.restype = ctypes.c_int
+        ll = ctypes.c_longlong
+        lib.oracle_bh_forces.argtypes = [i32, vp, vp, vp, vp, i32, i32, dbl, dbl, dbl, vp, vp]
+        lib.oracle_bh_forces.restype = ctypes.c_int
+        lib.oracle_bh_layout.argtypes = [i32, vp, vp, vp, i32, i32, dbl, dbl, dbl, dbl, dbl, i32,
+                                         dbl, vp, vp, vp]
+        lib.oracle_bh_layout.restype = ctypes.c_int
+        lib.oracle_bh_tree.argtypes = [i32, vp, i32] + [vp] * 10
+        lib.oracle_bh_tree.restype = ctypes.c_int
+        del ll
         _lib = lib
         return lib
 
@@ -123,3 +133,70 @@ def apply_update(ci, f, step, precision="f64"):
     q = np.zeros(1, dtype=dt)
     getattr(lib, f"oracle_apply_update_{precision}")(_ptr(c), float(f[0]), float(f[1]), float(step), _ptr(q))
     return c, float(q[0])
+
+
+# ------------------------------------------------------------ BatchLayoutBH
+THETA_PAPER = 1.2  # MAC threshold
+
+
+def bh_layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0, cooling=0.999,
+              theta=THETA_PAPER, max_batches=0, tol=0.0):
+    """Alg. S3 (BatchLayoutBH) from xy0.  Returns (xy (n,2) fp64, energy,
+    iters_done, node visits)."""
+    lib = _load()
+    xy = np.ascontiguousarray(np.asarray(xy0, dtype=np.float64).reshape(n, 2)).copy()
+    rowptr, colidx = _csr(rowptr, colidx)
+    energy = np.zeros(max(iters, 1), dtype=np.float64)
+    done = ctypes.c_int32(0)
+    visits = ctypes.c_longlong(0)
+    rc = lib.oracle_bh_layout(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0,
+                              cooling, theta, max_batches, tol, _ptr(energy), ctypes.byref(done),
+                              ctypes.byref(visits))
+    if rc != 0:
+        raise ValueError("oracle_bh_layout: invalid arguments")
+    return xy, energy[:int(done.value) if tol > 0 else iters], int(done.value), int(visits.value)
+
+
+def bh_forces(n, rowptr, colidx, snap, live, first=0, count=None, *, K=1.0, C=1.0,
+              theta=THETA_PAPER):
+    """Forces of Alg. S3 lines 13-19 for [first, first+count): tree built from
+    `snap` (rounded to fp32), live coordinates `live`.  Returns ((count,2)
+    fp64, node visits)."""
+    lib = _load()
+    if count is None:
+        count = n - first
+    s = np.ascontiguousarray(np.asarray(snap, dtype=np.float32).reshape(n, 2))
+    c = np.ascontiguousarray(np.asarray(live, dtype=np.float64).reshape(n, 2))
+    rowptr, colidx = _csr(rowptr, colidx)
+    out = np.zeros((max(count, 1), 2), dtype=np.float64)
+    visits = ctypes.c_longlong(0)
+    rc = lib.oracle_bh_forces(n, _ptr(rowptr), _ptr(colidx), _ptr(s), _ptr(c), first, count, K, C,
+                              theta, _ptr(out), ctypes.byref(visits))
+    if rc != 0:
+        raise ValueError("oracle_bh_forces: invalid arguments")
+    return out[:count], int(visits.value)
+
+
+def bh_tree(xy):
+    """The quadtree of Alg. S1 for fp32 coordinates xy (n,2), pre-order.
+    Returns a dict of node arrays plus the sorted codes, permutation and D."""
+    lib = _load()
+    xy = np.ascontiguousarray(np.asarray(xy, dtype=np.float32))
+    n = xy.shape[0]
+    cap = 17 * n + 1
+    a = {k: np.zeros(cap, np.int32) for k in ("level", "start", "count", "nchild")}
+    child = np.zeros(4 * cap, np.int32)
+    cx = np.zeros(cap, np.float32)
+    cy = np.zeros(cap, np.float32)
+    codes = np.zeros(n, np.uint32)
+    perm = np.zeros(n, np.int32)
+    D = ctypes.c_float(0)
+    nn = lib.oracle_bh_tree(n, _ptr(xy), cap, _ptr(a["level"]), _ptr(a["start"]), _ptr(a["count"]),
+                            _ptr(a["nchild"]), _ptr(child), _ptr(cx), _ptr(cy), _ptr(codes),
+                            _ptr(perm), ctypes.byref(D))
+    if nn < 0:
+        raise ValueError("oracle_bh_tree failed")
+    out = {k: v[:nn] for k, v in a.items()}
+    out.update(child=child[:4 * nn].reshape(nn, 4), cx=cx[:nn], cy=cy[:nn], codes=codes,
+               perm=perm, D=float(D.value))
+    return out

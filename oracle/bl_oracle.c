@@ -23,6 +23,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -42,6 +43,9 @@
 #undef REAL
 #undef SFX
 #undef SQRT
+
+/* BatchLayoutBH (Alg. S1-S3), fp64 force terms, fp32 decisions */
+#include "bl_oracle_bh.h"
 
 int oracle_max_threads(void) {
 #ifdef _OPENMP

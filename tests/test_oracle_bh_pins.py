@@ -1,0 +1,210 @@
+"""Pins of the BatchLayoutBH oracle (Alg. S1-S3, §3.5
+P:739-784) against things other than itself: the exact method (theta = 0),
+an independent geometric brute force on tiny graphs, hand-derived Morton
+codes and a closed-form far-cluster force, tree invariants, and the
+approximation's monotonicity and accuracy.  Readings B1-B9: DESIGN.md §3.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from blgen import edges_to_csr, grid_graph, rmat_graph, uniform_coords
+from tests import bruteforce
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "bh_examples.txt")
+
+
+def _random_graph(n, p, seed):
+    rng = np.random.default_rng(seed)
+    u, v = np.triu_indices(n, 1)
+    keep = rng.random(u.size) < p
+    return edges_to_csr(n, u[keep], v[keep])
+
+
+@pytest.mark.parametrize("b", [1, 7, 64, 10_000])
+def test_theta_zero_is_the_exact_method_with_neighbour_repulsion(b):
+    """B5: with theta = 0 the MAC never fires, every leaf term uses the live
+    coordinates, so BatchLayoutBH is exactly Alg. 2 with adjacent pairs also
+    repelling (Alg. S3 adds the tree repulsion over all vertices, B3)."""
+    g = rmat_graph(8, 4, 0.57, 0.19, 0.19, seed=2)
+    xy0 = uniform_coords(g.n, 3)
+    bh, Eb, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=3, batch=b, theta=0.0)
+    ex, Ee, _ = oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=3, batch=b,
+                              flags=oracle.REPULSE_NEIGHBORS)
+    ext = np.ptp(ex, axis=0).max()
+    assert np.abs(bh - ex).max() <= 1e-10 * ext
+    np.testing.assert_allclose(Eb, Ee, rtol=1e-10)
+
+
+@pytest.mark.parametrize("n,theta,b", [(5, 0.5, 1), (7, 1.2, 3), (9, 1.2, 9), (12, 0.8, 4),
+                                       (12, 2.0, 5)])
+def test_matches_geometric_bruteforce(n, theta, b):
+    """The C oracle (Morton codes, sorting, pre-order recursion) against the
+    independent geometric quadtree of tests/bruteforce.py."""
+    g = _random_graph(n, 0.35, seed=n)
+    rng = np.random.default_rng(100 + n)
+    # clustered points so that some cells are accepted even at small n
+    xy0 = np.concatenate([rng.random((n // 2, 2)) * 0.05,
+                          5.0 + rng.random((n - n // 2, 2))]).astype(np.float32)
+    A = bruteforce.dense_adj(n, g.rowptr, g.colidx)
+    ref_c, ref_E = bruteforce.bh_layout(n, A, xy0.tolist(), 4, b, theta)
+    got, E, _, _ = oracle.bh_layout(n, g.rowptr, g.colidx, xy0, iters=4, batch=b, theta=theta)
+    np.testing.assert_allclose(got, np.array(ref_c), rtol=0, atol=1e-12 * (1 + np.abs(got).max()))
+    np.testing.assert_allclose(E, ref_E, rtol=1e-12)
+
+
+def test_some_centroids_are_accepted_in_the_bruteforce_cases():
+    """Guard for the test above: at theta = 1.2 the clustered layout really
+    exercises the MAC (fewer visits than the full tree)."""
+    n = 12
+    g = _random_graph(n, 0.35, seed=n)
+    rng = np.random.default_rng(100 + n)
+    xy0 = np.concatenate([rng.random((n // 2, 2)) * 0.05,
+                          5.0 + rng.random((n - n // 2, 2))]).astype(np.float32)
+    _, v0 = oracle.bh_forces(n, g.rowptr, g.colidx, xy0, xy0, theta=0.0)
+    _, v1 = oracle.bh_forces(n, g.rowptr, g.colidx, xy0, xy0, theta=1.2)
+    assert v1 < v0
+
+
+def _golden_codes():
+    rows = []
+    with open(GOLDEN) as fh:
+        for line in fh:
+            line = line.split("#")[0].strip()
+            if line.startswith("code "):
+                lhs, rhs = line[5:].split("->")
+                x, y = (float(t) for t in lhs.split())
+                rows.append((x, y, int(rhs.strip(), 16)))
+    assert rows
+    return rows
+
+
+def test_morton_codes_worked_example():
+    """Hand-derived codes (tests/golden/bh_examples.txt): the unit square's
+    corners fix the box (D = 1, scale 65536), each point's 16-bit cell
+    indices are interleaved x -> even bits, y -> odd bits (B6)."""
+    rows = _golden_codes()
+    xy = np.array([[x, y] for x, y, _ in rows], np.float32)
+    t = oracle.bh_tree(xy)
+    assert t["D"] == 1.0
+    code_of = {int(v): int(c) for v, c in zip(t["perm"], t["codes"])}
+    for v, (_, _, want) in enumerate(rows):
+        assert code_of[v] == want, (rows[v], hex(code_of[v]), hex(want))
+    # Morton order = ascending codes, ties by vertex id
+    assert np.all(np.diff(t["codes"].astype(np.int64)) >= 0)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tree_invariants(seed):
+    """Alg. S1 structure: counts add up, children partition the parent's
+    Morton-contiguous range in order, levels step by one, leaves are single
+    vertices or level-16 multi-vertex leaves, the root centroid is the mean,
+    every vertex sits in exactly one leaf."""
+    rng = np.random.default_rng(seed)
+    n = 500
+    xy = np.concatenate([rng.random((n - 20, 2)), np.repeat(rng.random((4, 2)), 5, axis=0)])
+    xy = xy.astype(np.float32)                     # 4 groups of 5 coincident points
+    t = oracle.bh_tree(xy)
+    lv, st, cnt, nch, ch = t["level"], t["start"], t["count"], t["nchild"], t["child"]
+    assert cnt[0] == n and st[0] == 0 and lv[0] == 0
+    leaf_vertices = 0
+    for k in range(len(lv)):
+        if nch[k] == 0:
+            assert cnt[k] == 1 or lv[k] == 16
+            leaf_vertices += cnt[k]
+            if cnt[k] > 1:
+                codes = t["codes"][st[k]:st[k] + cnt[k]]
+                assert np.all(codes == codes[0])
+        else:
+            kids = ch[k, :nch[k]]
+            assert cnt[kids].sum() == cnt[k]
+            assert st[kids[0]] == st[k]
+            assert np.all(st[kids[1:]] == st[kids[:-1]] + cnt[kids[:-1]])
+            assert np.all(lv[kids] == lv[k] + 1)
+            assert np.all(kids > k)                 # pre-order: parent first
+    assert leaf_vertices == n
+    mean = xy.astype(np.float64).mean(0)
+    np.testing.assert_allclose([t["cx"][0], t["cy"][0]], mean, rtol=1e-6)
+
+
+def test_far_cluster_is_one_count_weighted_term():
+    """Closed form for B1/B2: a query at the origin and 4 points around
+    (100, 0).  The root is opened (D/d ~ 100.3/80 > 1.2); the cluster's
+    level-1 cell has D/d ~ 0.5 < 1.2 and is accepted, so the repulsion on the
+    query is exactly 4 x f_r at the cluster's centroid:
+    -4 C K^2 (r - q)/|r - q|^2."""
+    pts = np.array([[0.0, 0.0], [100.0, 0.3], [100.3, -0.3], [99.9, 0.1], [100.2, 0.0]],
+                   np.float32)
+    n = len(pts)
+    g = edges_to_csr(n, np.array([], np.int64), np.array([], np.int64))
+    K, C = 1.5, 0.7
+    f, visits = oracle.bh_forces(n, g.rowptr, g.colidx, pts, pts, 0, 1, K=K, C=C, theta=1.2)
+    r = np.array([np.float32(pts[1:, 0].astype(np.float64).mean()),
+                  np.float32(pts[1:, 1].astype(np.float64).mean())], np.float64)
+    d = r - pts[0]
+    want = -4 * C * K * K * d / (d @ d)
+    np.testing.assert_allclose(f[0], want, rtol=1e-12)
+    assert visits == 3                              # root, query leaf, cluster cell
+    # theta = 0: the four exact pair terms instead
+    f0, _ = oracle.bh_forces(n, g.rowptr, g.colidx, pts, pts, 0, 1, K=K, C=C, theta=0.0)
+    dd = pts[1:].astype(np.float64) - pts[0]
+    exact = -(C * K * K * dd / (dd * dd).sum(1, keepdims=True)).sum(0)
+    np.testing.assert_allclose(f0[0], exact, rtol=1e-12)
+
+
+def test_visits_non_increasing_in_theta():
+    g = grid_graph(30, 30)
+    xy = uniform_coords(g.n, 4)
+    v = [oracle.bh_forces(g.n, g.rowptr, g.colidx, xy, xy, 0, 200, theta=th)[1]
+         for th in (0.0, 0.3, 0.6, 0.9, 1.2, 2.0)]
+    assert all(a >= b for a, b in zip(v, v[1:])), v
+    assert v[0] > 5 * v[4]
+
+
+@pytest.mark.parametrize("theta,bound", [(0.5, 0.01), (1.2, 0.10)])
+def test_repulsion_accuracy_on_uniform_points(theta, bound):
+    """Mean relative error of the BH repulsion against the exact sum on
+    n = 2000 uniform points (no edges): <= 1% at theta = 0.5 and <= 10% at the
+    paper's 1.2 (SPEC.md acceptance 4's tolerance, which is ours: the paper
+    claims layout quality, not a force error)."""
+    n = 2000
+    g = edges_to_csr(n, np.array([], np.int64), np.array([], np.int64))
+    xy = uniform_coords(n, 5)
+    fb, _ = oracle.bh_forces(n, g.rowptr, g.colidx, xy, xy, theta=theta)
+    fe = oracle.forces(n, g.rowptr, g.colidx, xy)          # exact (no edges: all repel)
+    rel = np.hypot(*(fb - fe).T) / np.hypot(*fe.T)
+    assert rel.mean() <= bound, rel.mean()
+
+
+def test_degenerate_inputs():
+    # n = 1: no forces, no move
+    g1 = edges_to_csr(1, np.array([], np.int64), np.array([], np.int64))
+    xy, E, _, _ = oracle.bh_layout(1, g1.rowptr, g1.colidx, [[0.3, 0.4]], iters=2, batch=1)
+    assert np.array_equal(xy, [[0.3, 0.4]]) and np.all(E == 0)
+    # all coincident: D = 0, one multi-vertex leaf, every pair has d = 0
+    g = grid_graph(4, 5)
+    xy0 = np.full((g.n, 2), 0.25, np.float32)
+    t = oracle.bh_tree(xy0)
+    assert t["D"] == 0.0 and len(t["level"]) == 17 and t["count"][-1] == g.n
+    xy, E, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=2, batch=7)
+    assert np.array_equal(xy, xy0.astype(np.float64)) and np.all(E == 0)
+
+
+def test_one_batch_leaves_the_rest_unchanged_and_tree_is_per_iteration():
+    """Batch semantics (Alg. S3 lines 12-24) and B5: after one batch only the
+    batch moved; the second iteration's forces come from a tree of the
+    coordinates at ITS start (checked through bh_forces with that snapshot)."""
+    g = grid_graph(12, 12)
+    xy0 = uniform_coords(g.n, 6)
+    one, _, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=1, batch=40,
+                                    max_batches=1)
+    assert np.array_equal(one[40:], xy0[40:].astype(np.float64))
+    it1, _, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=1, batch=g.n)
+    it2, _, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=2, batch=g.n)
+    f, _ = oracle.bh_forces(g.n, g.rowptr, g.colidx, it1.astype(np.float32), it1)
+    step = 0.999
+    want = it1 + step * f / np.hypot(*f.T)[:, None]
+    np.testing.assert_allclose(it2, want, rtol=0, atol=1e-12)
