@@ -42,6 +42,16 @@ enum {
   BL_REPULSE_NEIGHBORS = 1u << 0
 };
 
+/* repulsion algorithm (bl_params.algo) */
+enum {
+  BL_ALGO_EXACT = 0, /* exact all-pairs repulsion: BatchLayout, Alg. 2          */
+  BL_ALGO_BH = 1     /* Barnes-Hut quadtree repulsion: BatchLayoutBH, Alg. S1-S3
+                        (§3.5).  Per Alg. S3 adjacent pairs attract
+                        AND repel (BL_REPULSE_NEIGHBORS is implied; flags are ignored).
+                        The tree is rebuilt from the coordinates at every iteration start;
+                        readings B1-B9 in DESIGN.md §3.                                   */
+};
+
 typedef struct {
   int32_t iters;       /* >= 0; MaxIteration of Alg. 2. 0 = no-op      */
   int32_t batch;       /* >= 1; BS of Alg. 2. > n is clamped to n  */
@@ -58,11 +68,15 @@ typedef struct {
   int32_t max_batches; /* > 0: stop after that many batch updates in total
                           (debug / one-batch parity); <= 0: no limit           */
   uint32_t flags;      /* BL_REPULSE_NEIGHBORS                                 */
+  int32_t algo;        /* BL_ALGO_EXACT (default) or BL_ALGO_BH                */
+  float theta;         /* BL_ALGO_BH: MAC threshold, accept a cell when
+                          theta > D_cell / d; >= 0, 0 = exact; the
+                          paper's value 1.2 is the default             */
 } bl_params;
 
 /* Fill p with the paper's defaults: iters 600 (the CLI default),
  * batch 256, K = 1, C = 1, step0 = 1.0, cooling = 0.999, tol = 0,
- * max_batches = 0, flags = 0. */
+ * max_batches = 0, flags = 0, algo = BL_ALGO_EXACT, theta = 1.2. */
 void bl_params_default(bl_params *p);
 
 /* Create a context on the current CUDA device for the undirected graph G
@@ -103,9 +117,16 @@ bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t trace_len,
 /* Debug / parity: the raw combined forces f(i, c) of §2.2 for
  * i in [first, first+count) at the device state d_xy (not modified), written
  * to d_f_out (float2[count], device).  Uses the same device code as the
- * layout kernel.  Only p->K, p->C and p->flags are read. */
+ * layout kernel.  Only p->K, p->C, p->flags, p->algo and p->theta are read
+ * (BL_ALGO_BH: the tree is built from d_xy itself). */
 bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int32_t count, float *d_f_out,
                     const bl_params *p, void *cuda_stream);
+
+/* BL_ALGO_BH: number of quadtree nodes the last bl_layout_device /
+ * bl_layout / bl_forces call visited in Alg. S2 traversals (summed over all
+ * queries; leaves and accepted or opened cells each count once).  Synchronises
+ * h's last stream.  *visits = 0 after an exact-algorithm call. */
+bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits);
 
 /* Largest n the resident design accepts on the current device. */
 int32_t bl_max_vertices(void);

@@ -14,6 +14,7 @@ _SO = os.path.join(_HERE, "libbl.so")
 
 BL_OK, BL_EINVAL, BL_ENOMEM, BL_ECUDA, BL_ESTATE = 0, -1, -2, -3, -4
 BL_REPULSE_NEIGHBORS = 1
+BL_ALGO_EXACT, BL_ALGO_BH = 0, 1
 
 
 class bl_params(ctypes.Structure):
@@ -27,6 +28,8 @@ class bl_params(ctypes.Structure):
         ("tol", ctypes.c_double),
         ("max_batches", ctypes.c_int32),
         ("flags", ctypes.c_uint32),
+        ("algo", ctypes.c_int32),
+        ("theta", ctypes.c_float),
     ]
 
 
@@ -59,6 +62,8 @@ def _load() -> ctypes.CDLL:
     lib.bl_max_vertices.restype = i32
     lib.bl_last_launch_count.argtypes = [vp]
     lib.bl_last_launch_count.restype = i32
+    lib.bl_last_visits.argtypes = [vp, P(ctypes.c_ulonglong)]
+    lib.bl_last_visits.restype = ctypes.c_int
     lib.bl_kernel_name.argtypes = [vp]
     lib.bl_kernel_name.restype = ctypes.c_char_p
     lib.bl_microbench.argtypes = [P(ctypes.c_double)]
@@ -78,7 +83,7 @@ lib = _load()
 
 # symbols include/bl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bl_params_default", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
-           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_kernel_name", "bl_microbench",
+           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_microbench",
            "bl_debug_profile", "bl_destroy", "bl_status_string", "bl_last_error")
 
 
@@ -162,6 +167,12 @@ def bl_max_vertices() -> int:
 
 def bl_last_launch_count(h: int) -> int:
     return int(lib.bl_last_launch_count(h))
+
+
+def bl_last_visits(h: int) -> int:
+    v = ctypes.c_ulonglong(0)
+    _check(lib.bl_last_visits(h, ctypes.byref(v)), h)
+    return int(v.value)
 
 
 def bl_kernel_name(h: int) -> str:

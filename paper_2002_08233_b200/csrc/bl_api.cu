@@ -17,6 +17,7 @@
 
 #include "../../include/bl.h"
 #include "bl_kernel.cuh"
+#include "bl_bh.cuh"
 
 #ifndef BL_DEFAULT_NT
 #define BL_DEFAULT_NT 512
@@ -63,6 +64,18 @@ struct bl_ctx {
   int32_t launches = 0;
   std::string err;
   char kname[64] = {0};
+  // BatchLayoutBH scratch (allocated on first use, sized by n)
+  bool bh_ready = false;
+  unsigned *d_keyA = nullptr, *d_keyB = nullptr, *d_hist = nullptr;
+  int *d_valA = nullptr, *d_valB = nullptr, *d_cnt = nullptr, *d_off = nullptr, *d_blk = nullptr;
+  int *d_nnodes = nullptr;
+  float4 *d_bbox = nullptr, *d_nodeA = nullptr;
+  float2 *d_snap = nullptr, *d_fb = nullptr;
+  size_t fb_cap = 0;
+  int4 *d_nodeB = nullptr, *d_nodeC = nullptr;
+  double2 *d_nsum = nullptr;
+  unsigned long long *d_visits = nullptr;
+  bool last_bh = false;
 };
 
 static thread_local std::string g_create_err;
@@ -99,6 +112,8 @@ extern "C" void bl_params_default(bl_params *p) {
   p->tol = 0.0;
   p->max_batches = 0;
   p->flags = 0;
+  p->algo = BL_ALGO_EXACT;
+  p->theta = 1.2f;
 }
 
 extern "C" const char *bl_status_string(bl_status s) {
@@ -300,6 +315,23 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_bar);
   cudaFree(h->d_prof);
   cudaFree(h->d_xy_host_path);
+  cudaFree(h->d_keyA);
+  cudaFree(h->d_keyB);
+  cudaFree(h->d_hist);
+  cudaFree(h->d_valA);
+  cudaFree(h->d_valB);
+  cudaFree(h->d_cnt);
+  cudaFree(h->d_off);
+  cudaFree(h->d_blk);
+  cudaFree(h->d_nnodes);
+  cudaFree(h->d_bbox);
+  cudaFree(h->d_nodeA);
+  cudaFree(h->d_snap);
+  cudaFree(h->d_fb);
+  cudaFree(h->d_nodeB);
+  cudaFree(h->d_nodeC);
+  cudaFree(h->d_nsum);
+  cudaFree(h->d_visits);
   delete h;
 }
 
@@ -313,6 +345,9 @@ static bl_status check_params(bl_ctx *h, const bl_params *p) {
   if (!(p->cooling > 0.0 && p->cooling <= 1.0)) return fail(h, BL_EINVAL, "cooling must be in (0,1]");
   if (!(p->tol >= 0.0) || !std::isfinite(p->tol)) return fail(h, BL_EINVAL, "tol must be >= 0");
   if (p->flags & ~(uint32_t)BL_REPULSE_NEIGHBORS) return fail(h, BL_EINVAL, "unknown flags");
+  if (p->algo != BL_ALGO_EXACT && p->algo != BL_ALGO_BH) return fail(h, BL_EINVAL, "unknown algo");
+  if (p->algo == BL_ALGO_BH && (!(p->theta >= 0.f) || !std::isfinite(p->theta)))
+    return fail(h, BL_EINVAL, "theta must be >= 0");
   return BL_OK;
 }
 
@@ -415,6 +450,114 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   return BL_OK;
 }
 
+// BatchLayoutBH: one cooperative launch of bl_bh_kernel (csrc/bl_bh.cuh).
+static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
+                           int forces_mode, int first, int count, float2 *f_out) {
+  const int n = h->n, G = h->num_sms;
+  const int b = forces_mode ? std::max(1, count) : std::min(p->batch, n);
+  bl_status s;
+  if (!h->bh_ready) {
+    const size_t cap = (size_t)17 * n + 1;  // <= 17 nodes per sorted position
+#define ALLOC(ptr, cnt)                                                                       \
+  do {                                                                                        \
+    cudaError_t e_ = cudaMalloc((void **)&(ptr), sizeof(*(ptr)) * (size_t)(cnt));             \
+    if (e_ != cudaSuccess) return fail(h, BL_ENOMEM, "cudaMalloc %s: %s", #ptr, cudaGetErrorString(e_)); \
+  } while (0)
+    ALLOC(h->d_keyA, n);
+    ALLOC(h->d_keyB, n);
+    ALLOC(h->d_valA, n);
+    ALLOC(h->d_valB, n);
+    ALLOC(h->d_hist, 256 * G);
+    ALLOC(h->d_bbox, G);
+    ALLOC(h->d_cnt, n);
+    ALLOC(h->d_off, n + 1);
+    ALLOC(h->d_blk, G);
+    ALLOC(h->d_snap, n);
+    ALLOC(h->d_nodeA, cap);
+    ALLOC(h->d_nodeB, cap);
+    ALLOC(h->d_nodeC, cap);
+    ALLOC(h->d_nsum, cap);
+    ALLOC(h->d_nnodes, 1);
+    ALLOC(h->d_visits, G);
+#undef ALLOC
+    h->bh_ready = true;
+  }
+  if ((s = grow(h, h->d_fb, h->fb_cap, (size_t)b)) != BL_OK) return s;
+  if (!h->d_e_cta) {
+    size_t cap = 0;
+    if ((s = grow(h, h->d_e_cta, cap, (size_t)2 * G)) != BL_OK) return s;
+  }
+  if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
+  BHKParams k{};
+  k.n = n;
+  k.b = b;
+  k.nb = (n + b - 1) / b;
+  k.iters = p->iters;
+  k.max_batches = p->max_batches;
+  k.ck2 = p->C * p->K * p->K;
+  k.invK = 1.0f / p->K;
+  const float th = p->theta;
+  k.theta2 = th * th;  // fp32, as the oracle (reading B7)
+  k.step0 = p->step0;
+  k.cooling = p->cooling;
+  k.tol = p->tol;
+  k.forces_mode = forces_mode;
+  k.first = first;
+  k.count = count;
+  k.xy = d_xy;
+  k.rowptr = h->d_rowptr;
+  k.colidx = h->d_colidx;
+  k.keyA = h->d_keyA;
+  k.keyB = h->d_keyB;
+  k.valA = h->d_valA;
+  k.valB = h->d_valB;
+  k.hist = h->d_hist;
+  k.bbox = h->d_bbox;
+  k.cnt = h->d_cnt;
+  k.off = h->d_off;
+  k.blk = h->d_blk;
+  k.snap = h->d_snap;
+  k.nodeA = h->d_nodeA;
+  k.nodeB = h->d_nodeB;
+  k.nodeC = h->d_nodeC;
+  k.nsum = h->d_nsum;
+  k.nnodes = h->d_nnodes;
+  k.fb = h->d_fb;
+  k.e_cta = h->d_e_cta;
+  k.energy = h->d_energy;
+  k.iters_done = h->d_iters_done;
+  k.bar = h->d_bar;
+  k.f_out = f_out;
+  k.visits = h->d_visits;
+  void *kfn = (void *)bl_bh_kernel<BH_NT>;
+  const size_t smem = sizeof(BHShared);
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return fail(h, BL_ECUDA, "bh smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
+  int occ = 0;
+  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, BH_NT, smem));
+  if (occ < 1) return fail(h, BL_ECUDA, "bh kernel does not fit an SM");
+  BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_visits, 0, sizeof(unsigned long long) * G, st));
+  void *args[] = {&k};
+  BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(BH_NT), args, smem, st));
+  h->launches = 1;
+  h->last_bh = true;
+  return BL_OK;
+}
+
+extern "C" bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits) {
+  if (!h || !visits) return fail(h, BL_EINVAL, "NULL argument");
+  *visits = 0;
+  if (!h->last_bh || !h->d_visits) return BL_OK;
+  BL_CUDA(h, cudaStreamSynchronize(h->last_stream));
+  std::vector<unsigned long long> v(h->num_sms);
+  BL_CUDA(h, cudaMemcpy(v.data(), h->d_visits, sizeof(unsigned long long) * v.size(),
+                        cudaMemcpyDeviceToHost));
+  for (auto x : v) *visits += x;
+  return BL_OK;
+}
+
 extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p, void *cuda_stream) {
   if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
   h->launches = 0;
@@ -429,7 +572,9 @@ extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p
     h->have_layout = false;
     return BL_OK;
   }
-  s = launch(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr);
+  h->last_bh = false;
+  s = p->algo == BL_ALGO_BH ? launch_bh(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr)
+                            : launch(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr);
   if (s != BL_OK) return s;
   h->have_layout = true;
   return BL_OK;
@@ -491,6 +636,12 @@ extern "C" bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int3
   if (first < 0 || count < 0 || first > h->n - count)
     return fail(h, BL_EINVAL, "range [%d, %d+%d) outside [0, %d)", first, first, count, h->n);
   if (count == 0) return BL_OK;
-  return launch(h, const_cast<float2 *>(reinterpret_cast<const float2 *>(d_xy)), p,
-                (cudaStream_t)cuda_stream, 1, first, count, reinterpret_cast<float2 *>(d_f_out));
+  h->last_stream = (cudaStream_t)cuda_stream;
+  h->last_bh = false;
+  float2 *xy2 = const_cast<float2 *>(reinterpret_cast<const float2 *>(d_xy));
+  if (p->algo == BL_ALGO_BH)
+    return launch_bh(h, xy2, p, (cudaStream_t)cuda_stream, 1, first, count,
+                     reinterpret_cast<float2 *>(d_f_out));
+  return launch(h, xy2, p, (cudaStream_t)cuda_stream, 1, first, count,
+                reinterpret_cast<float2 *>(d_f_out));
 }

@@ -35,7 +35,7 @@ def gpu_layout(g, xy0, *, device_path=True, **params):
     return xy, trace, done
 
 
-def gpu_forces(g, xy, first=0, count=None, **params):
+def gpu_forces(g, xy, first=0, count=None, with_visits=False, **params):
     import torch
 
     import paper_2002_08233_b200 as bl
@@ -43,7 +43,10 @@ def gpu_forces(g, xy, first=0, count=None, **params):
         d = torch.from_numpy(np.ascontiguousarray(xy, dtype=np.float32).copy()).cuda()
         f = lay.forces(d, first, count, **params)
         torch.cuda.synchronize()
-        return f.cpu().numpy().astype(np.float64)
+        out = f.cpu().numpy().astype(np.float64)
+        if with_visits:
+            return out, bl.bl_last_visits(lay.h)
+        return out
 
 
 def assert_positions_close(got, ref, tol=POS_TOL, what=""):
