@@ -319,12 +319,46 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
             "value": pairs / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
             "sample": f"first {k} batch update(s) of iteration 0 of {name} (b={b}), {dt:.1f} s",
         }
+    if not args.no_bh:
+        line["bh"] = bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, t_local / args.steps)
     lay.close()
     if args.prof and rank == 0:
         line["phase_profile"] = phase_profile(g, xy0, params, dev, clocks.get("sm_mhz") or sm_max)
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, exact_s):
+    """Secondary line: BatchLayoutBH (algo = BL_ALGO_BH, Alg. S1-S3, theta =
+    1.2 of P:869) on the same workload, same timing rules (L2 flushed, CUDA
+    events on the launching stream, >= 1 warm-up)."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    p = dict(params, algo=bl.BL_ALGO_BH, theta=args.theta)
+    d_xy = torch.empty_like(d_xy0)
+    steps = max(2, args.steps)
+    for _ in range(max(1, min(args.warmup, 2))):
+        d_xy.copy_(d_xy0)
+        lay.layout_device(d_xy, stream=stream, **p)
+    torch.cuda.synchronize()
+    ms = []
+    for i in range(steps):
+        d_xy.copy_(d_xy0)
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        lay.layout_device(d_xy, stream=stream, **p)
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    visits = bl.bl_last_visits(lay.h)
+    t = sum(ms) / 1e3 / steps
+    return {"algo": f"BatchLayoutBH (Alg. S3), theta {args.theta}", "kernel": "bl_bh_kernel<512>",
+            "iters_per_sec": cfg.iters / t, "ms_per_step": 1e3 * t, "steps": steps,
+            "visits_per_step": visits, "visits_per_sec": visits / t,
+            "speedup_vs_exact": exact_s / t, "gpu_launches_per_step": bl.bl_last_launch_count(lay.h)}
 
 
 def phase_profile(g, xy0, params, dev, mhz):
@@ -363,6 +397,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", default="nccl")
     ap.add_argument("--prof", action="store_true", help="add a phase profile (extra untimed run)")
+    ap.add_argument("--no-bh", action="store_true", help="skip the secondary BatchLayoutBH line")
+    ap.add_argument("--theta", type=float, default=1.2, help="BatchLayoutBH MAC threshold (P:869)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

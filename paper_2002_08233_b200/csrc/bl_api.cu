@@ -76,6 +76,8 @@ struct bl_ctx {
   double2 *d_nsum = nullptr;
   unsigned long long *d_visits = nullptr;
   bool last_bh = false;
+  float2 *d_attr_bh = nullptr;
+  unsigned *d_aflag = nullptr;
 };
 
 static thread_local std::string g_create_err;
@@ -332,6 +334,8 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_nodeC);
   cudaFree(h->d_nsum);
   cudaFree(h->d_visits);
+  cudaFree(h->d_attr_bh);
+  cudaFree(h->d_aflag);
   delete h;
 }
 
@@ -479,10 +483,12 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
     ALLOC(h->d_nsum, cap);
     ALLOC(h->d_nnodes, 1);
     ALLOC(h->d_visits, G);
+    ALLOC(h->d_attr_bh, std::max(1, h->n_items));
+    ALLOC(h->d_aflag, std::max(1, h->n_items));
 #undef ALLOC
     h->bh_ready = true;
   }
-  if ((s = grow(h, h->d_fb, h->fb_cap, (size_t)b)) != BL_OK) return s;
+  if ((s = grow(h, h->d_fb, h->fb_cap, (size_t)2 * b)) != BL_OK) return s;  // pend[2][b]
   if (!h->d_e_cta) {
     size_t cap = 0;
     if ((s = grow(h, h->d_e_cta, cap, (size_t)2 * G)) != BL_OK) return s;
@@ -522,7 +528,13 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.nodeC = h->d_nodeC;
   k.nsum = h->d_nsum;
   k.nnodes = h->d_nnodes;
-  k.fb = h->d_fb;
+  k.pend = h->d_fb;
+  k.prof = h->d_prof;
+  k.item_ptr = h->d_item_ptr;
+  k.item_v = h->d_item_v;
+  k.item_k0 = h->d_item_k0;
+  k.attr = h->d_attr_bh;
+  k.aflag = h->d_aflag;
   k.e_cta = h->d_e_cta;
   k.energy = h->d_energy;
   k.iters_done = h->d_iters_done;
@@ -539,6 +551,7 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
   BL_CUDA(h, cudaMemsetAsync(h->d_visits, 0, sizeof(unsigned long long) * G, st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_aflag, 0, sizeof(unsigned) * std::max(1, h->n_items), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(BH_NT), args, smem, st));
   h->launches = 1;

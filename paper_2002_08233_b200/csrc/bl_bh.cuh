@@ -56,13 +56,20 @@ struct BHKParams {
   int4 *nodeC;        // [cap] children (-1 padded)
   double2 *nsum;      // [cap] fp64 coordinate sums
   int *nnodes;        // [1]
-  float2 *fb;         // [b] forces of the running batch
   double *e_cta;      // [G]
   double *energy;     // [iters]
   int *iters_done;
   unsigned *bar;
   float2 *f_out;
   unsigned long long *visits;  // [G] node visits per CTA (for the roofline)
+  float2 *pend;                // [2][b] new coordinates of the last two batches
+  // attraction of high-degree ("split") vertices, edge-parallel: rows cut in
+  // items of <= BL_ECH entries (the context's item lists), one partial per
+  // item, published with a release flag stamped with the batch number
+  const int *item_ptr, *item_v, *item_k0;
+  float2 *attr;                // [n_items]
+  unsigned *aflag;             // [n_items]
+  unsigned long long *prof;    // optional phase profile (BL_PROFILE=1)
 };
 
 struct BHShared {
@@ -143,7 +150,7 @@ __device__ __forceinline__ int bh_block_scan(int v, BHShared &sh, int *total) {
 // ---------------------------------------------------------------- build
 template <int NT>
 __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_target,
-                              int *unit_dummy) {
+                              int *unit_dummy, BLProf &pf) {
   const int G = gridDim.x, c = blockIdx.x, n = p.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int lo, hi;
@@ -180,24 +187,34 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
     }
   }
   bl_grid_sync(p.bar, bar_target, unit_dummy);
-  if (threadIdx.x == 0) {
-    float4 r = __ldcg(p.bbox);
-    for (int cc = 1; cc < G; ++cc) {
+  if (threadIdx.x < 32) {  // one warp, lanes strided over the CTAs (min/max: exact)
+    float4 r = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+    for (int cc = lane; cc < G; cc += 32) {
       const float4 q = __ldcg(p.bbox + cc);
       r.x = fminf(r.x, q.x);
       r.y = fmaxf(r.y, q.y);
       r.z = fminf(r.z, q.z);
       r.w = fmaxf(r.w, q.w);
     }
-    const float ex = __fsub_rn(r.y, r.x), ey = __fsub_rn(r.w, r.z);
-    const float D = ex > ey ? ex : ey;  // Alg. S3 line 7
-    sh.D = D;
-    sh.xmin = r.x;
-    sh.ymin = r.z;
-    sh.degenerate = !(D > 0.0f);
-    sh.scale = sh.degenerate ? 0.0f : __fdiv_rn(65536.0f, D);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r.x = fminf(r.x, __shfl_xor_sync(0xffffffffu, r.x, o));
+      r.y = fmaxf(r.y, __shfl_xor_sync(0xffffffffu, r.y, o));
+      r.z = fminf(r.z, __shfl_xor_sync(0xffffffffu, r.z, o));
+      r.w = fmaxf(r.w, __shfl_xor_sync(0xffffffffu, r.w, o));
+    }
+    if (lane == 0) {
+      const float ex = __fsub_rn(r.y, r.x), ey = __fsub_rn(r.w, r.z);
+      const float D = ex > ey ? ex : ey;  // Alg. S3 line 7
+      sh.D = D;
+      sh.xmin = r.x;
+      sh.ymin = r.z;
+      sh.degenerate = !(D > 0.0f);
+      sh.scale = sh.degenerate ? 0.0f : __fdiv_rn(65536.0f, D);
+    }
   }
   __syncthreads();
+  pf.mark(0);
 
   // B1: codes of the owned chunk (input order = vertex id order)
   for (int v = lo + threadIdx.x; v < hi; v += NT) {
@@ -219,20 +236,30 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += NT) p.hist[d * G + c] = sh.hist[d];
     bl_grid_sync(p.bar, bar_target, unit_dummy);
-    // global base of each digit for this CTA: digits below + CTAs below
+    // global base of each digit for this CTA: digits below + CTAs below.
+    // Warp w handles digits 16w..16w+15, lanes strided over the CTAs (all
+    // loads in flight at once); integer sums, so the order is immaterial.
     {
-      unsigned tot = 0, pre = 0;
-      const int d = threadIdx.x;
-      if (d < 256) {
-        for (int cc = 0; cc < G; ++cc) {
+      for (int j = 0; j < 256 / BH_NW; ++j) {
+        const int d = warp * (256 / BH_NW) + j;
+        unsigned tot = 0, pre = 0;
+        for (int cc = lane; cc < G; cc += 32) {
           const unsigned h = __ldcg(p.hist + d * G + cc);
-          if (cc < c) pre += h;
           tot += h;
+          if (cc < c) pre += h;
+        }
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        pre = __reduce_add_sync(0xffffffffu, pre);
+        if (lane == 0) {
+          sh.hist[d] = tot;
+          sh.base[d] = pre;
         }
       }
+      __syncthreads();
       int total;
-      const int ex = bh_block_scan(d < 256 ? (int)tot : 0, sh, &total);
-      if (d < 256) sh.base[d] = (unsigned)ex + pre;
+      const int d = threadIdx.x;
+      const int ex = bh_block_scan(d < 256 ? (int)sh.hist[d] : 0, sh, &total);
+      if (d < 256) sh.base[d] += (unsigned)ex;
     }
     __syncthreads();
     // stable scatter in tiles of NT consecutive elements
@@ -286,6 +313,7 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
     vout = tv;
   }
   // sorted (code, id) are in keyA / valA (4 passes)
+  pf.mark(1);
 
   // B3: node counts per sorted position, snapshot in sorted order
   int my = 0;
@@ -309,12 +337,14 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
   // exclusive offsets: CTAs below, then this CTA's positions in order.  Each
   // thread owns a contiguous run of the chunk so the scan is over runs.
   {
-    int before = 0, all = 0;
-    for (int cc = 0; cc < G; ++cc) {
-      const int s = __ldcg(p.blk + cc);
-      if (cc < c) before += s;
-      all += s;
+    unsigned bf = 0, al = 0;
+    for (int cc = lane; cc < G; cc += 32) {
+      const unsigned s = (unsigned)__ldcg(p.blk + cc);
+      if (cc < c) bf += s;
+      al += s;
     }
+    const int before = (int)__reduce_add_sync(0xffffffffu, bf);
+    const int all = (int)__reduce_add_sync(0xffffffffu, al);
     const int len = hi - lo;
     const int per = (len + NT - 1) / NT;
     const int a = lo + threadIdx.x * per, e = min(hi, a + per);
@@ -377,14 +407,15 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
         }
         p.nsum[k] = make_double2(sx, sy);
         p.nodeA[k] = make_float4((float)(sx / count), (float)(sy / count), 0.f, (float)count);
-        p.nodeC[k] = make_int4(-1, -1, -1, -1);
+        p.nodeC[k] = make_int4(-1, -1, -1, count == 1 ? __ldcg(p.valA + i) : -1);
       }
     }
   }
   bl_grid_sync(p.bar, bar_target, unit_dummy);
 
-  // B4': children lists of internal nodes (pre-order: first child k+1, then
-  // follow the children's skip pointers up to the parent's skip)
+  // B4': children lists of internal nodes (pre-order: child 0 is k+1, the
+  // next ones follow the children's skip pointers up to the parent's skip);
+  // stored as (c1, c2, c3, -1)
   for (int k = c * NT + threadIdx.x; k < Nn; k += G * NT) {
     int4 B = __ldcg(p.nodeB + k);
     if (B.x & (1 << 16)) continue;
@@ -394,12 +425,13 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
       ch[m++] = t;
       t = __ldcg(p.nodeB + t).w;
     }
-    p.nodeC[k] = make_int4(ch[0], ch[1], ch[2], ch[3]);
+    p.nodeC[k] = make_int4(ch[1], ch[2], ch[3], -1);
     B.x |= m << 8;
     p.nodeB[k] = B;
   }
   bl_grid_sync(p.bar, bar_target, unit_dummy);
 
+  pf.mark(2);
   // B5: centroids bottom-up (Alg. S1 line 11), fp64 sums in digit order
   const float D = sh.D;
   for (int L = 15; L >= 0; --L) {
@@ -407,10 +439,10 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
       const int4 B = __ldcg(p.nodeB + k);
       if ((B.x & 0xff) != L || (B.x & (1 << 16))) continue;
       const int4 C4 = __ldcg(p.nodeC + k);
-      const int chs[4] = {C4.x, C4.y, C4.z, C4.w};
+      const int chs[4] = {k + 1, C4.x, C4.y, C4.z};
+      const int m = (B.x >> 8) & 0xff;
       double sx = 0.0, sy = 0.0;
-      for (int q = 0; q < 4; ++q) {
-        if (chs[q] < 0) break;
+      for (int q = 0; q < m; ++q) {
         const double2 s = __ldcg(p.nsum + chs[q]);
         sx = sx + s.x;
         sy = sy + s.y;
@@ -422,17 +454,43 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
     }
     bl_grid_sync(p.bar, bar_target, unit_dummy);
   }
+  pf.mark(3);
 }
 
 // ---------------------------------------------------------------- forces
-// Exact repulsive terms of a leaf's vertices against vertex v at (qx, qy),
-// live coordinates (reading B5/B8/B9).
-__device__ __forceinline__ void bh_leaf_terms(const BHKParams &p, const int4 &B, int v, float qx,
-                                              float qy, float &fx, float &fy) {
-  for (int s = B.y; s < B.y + B.z; ++s) {
-    const int j = __ldcg(p.valA + s);
+// Tree records are read with plain (L1-cacheable) loads: they are written in
+// the build phase before a grid barrier whose acquire orders them, and the
+// top of the tree is shared by every query of the SM.
+struct BHNode {
+  float4 A;  // centroid x, y, D_L^2, count
+  int4 B;    // level | nchild << 8 | leaf << 16, start, count, skip
+  int4 C;    // children 1..3 (child 0 is k+1), vertex id of a single leaf
+};
+__device__ __forceinline__ BHNode bh_load(const BHKParams &p, int k) {
+  BHNode nd;
+  nd.A = p.nodeA[k];
+  nd.B = p.nodeB[k];
+  nd.C = p.nodeC[k];
+  return nd;
+}
+
+// Live coordinate of vertex j (reading B5): batch `pl` vertices [plo, phi)
+// hold their new coordinates in pend (committed to xy one batch later).
+__device__ __forceinline__ float2 bh_live(const BHKParams &p, int j, int plo, int phi,
+                                          const float2 *pend) {
+  return (j >= plo && j < phi) ? __ldcg(pend + (j - plo)) : __ldcg(p.xy + j);
+}
+
+// Exact repulsive terms of a leaf's vertices against vertex v at (qx, qy)
+// (readings B5/B8/B9).
+__device__ __forceinline__ void bh_leaf_terms(const BHKParams &p, const BHNode &nd, int v, float qx,
+                                              float qy, int plo, int phi, const float2 *pend,
+                                              float &fx, float &fy) {
+  const int cnt = nd.B.z;
+  for (int s = 0; s < cnt; ++s) {
+    const int j = cnt == 1 ? nd.C.w : __ldcg(p.valA + nd.B.y + s);
     if (j == v) continue;
-    const float2 cj = __ldcg(p.xy + j);
+    const float2 cj = bh_live(p, j, plo, phi, pend);
     const float dx = cj.x - qx, dy = cj.y - qy;
     const float d2 = fmaf(dx, dx, dy * dy);
     if (d2 > 0.f) {
@@ -458,35 +516,33 @@ __device__ __forceinline__ bool bh_mac(const BHKParams &p, const float4 &A, floa
 
 // One lane walks the subtree below node k (k's own MAC already failed) with
 // the skip pointers: no stack.
-__device__ __forceinline__ void bh_walk_subtree(const BHKParams &p, int k, int v, float qx, float qy,
+__device__ __forceinline__ void bh_walk_subtree(const BHKParams &p, int k, int end, int v, float qx,
+                                                float qy, int plo, int phi, const float2 *pend,
                                                 float &fx, float &fy, unsigned long long &vis) {
-  const int end = __ldcg(p.nodeB + k).w;
   int t = k + 1;
   while (t < end) {
-    const int4 B = __ldcg(p.nodeB + t);
+    const BHNode nd = bh_load(p, t);
     ++vis;
-    if (B.x & (1 << 16)) {
-      bh_leaf_terms(p, B, v, qx, qy, fx, fy);
-      t = B.w;
-    } else if (bh_mac(p, __ldcg(p.nodeA + t), qx, qy, fx, fy)) {
-      t = B.w;
+    if (nd.B.x & (1 << 16)) {
+      bh_leaf_terms(p, nd, v, qx, qy, plo, phi, pend, fx, fy);
+      t = nd.B.w;
+    } else if (bh_mac(p, nd.A, qx, qy, fx, fy)) {
+      t = nd.B.w;
     } else {
       t = t + 1;
     }
   }
 }
 
-// Force of vertex v (one warp): CSR attraction + Barnes-Hut repulsion.
-// Returns the warp-summed force on every lane.
-__device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh, int v,
-                                                unsigned long long &vis) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float2 cv = __ldcg(p.xy + v);
+// Attraction sum over CSR entries [k0, k1) of vertex v at cv (one warp,
+// lanes strided, fixed butterfly): f_a = d^2/K along the unit vector
+// (Alg. S3 lines 15-17), live neighbour coordinates.
+__device__ __forceinline__ float2 bh_attr_range(const BHKParams &p, int k0, int k1, float2 cv,
+                                                int plo, int phi, const float2 *pend) {
+  const int lane = threadIdx.x & 31;
   float fx = 0.f, fy = 0.f;
-  // attraction f_a = d^2/K along the unit vector (Alg. S3 lines 15-17)
-  const int k0 = __ldg(p.rowptr + v), k1 = __ldg(p.rowptr + v + 1);
   for (int k = k0 + lane; k < k1; k += 32) {
-    const float2 cj = __ldcg(p.xy + __ldg(p.colidx + k));
+    const float2 cj = bh_live(p, __ldg(p.colidx + k), plo, phi, pend);
     const float dx = cj.x - cv.x, dy = cj.y - cv.y;
     const float d2 = fmaf(dx, dx, dy * dy);
     if (d2 > 0.f) {
@@ -495,6 +551,61 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
       fy = fmaf(d * p.invK, dy, fy);
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+  }
+  return make_float2(fx, fy);
+}
+
+// Items of the split vertices in [vlo, vhi): warp gw of GW computes items
+// gw, gw + GW, ... and publishes each partial with a release flag.
+__device__ __forceinline__ void bh_attr_items(const BHKParams &p, int vlo, int vhi, int gw, int GW,
+                                              unsigned stamp, int plo, int phi,
+                                              const float2 *pend) {
+  const int lane = threadIdx.x & 31;
+  const int ib = __ldg(p.item_ptr + vlo), ie = __ldg(p.item_ptr + vhi);
+  for (int it = ib + gw; it < ie; it += GW) {
+    const int v = __ldg(p.item_v + it);
+    if (__ldg(p.item_ptr + v + 1) - __ldg(p.item_ptr + v) <= 1) continue;  // inline vertex
+    const int k0 = __ldg(p.item_k0 + it);
+    const int k1 = min(k0 + BL_ECH, __ldg(p.rowptr + v + 1));
+    const float2 f = bh_attr_range(p, k0, k1, __ldcg(p.xy + v), plo, phi, pend);
+    if (lane == 0) {
+      p.attr[it] = f;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.aflag + it), "r"(stamp) : "memory");
+    }
+  }
+}
+
+// Sum of the published item partials of split vertex v (waits for them).
+__device__ __forceinline__ float2 bh_attr_gather(const BHKParams &p, int v, unsigned stamp) {
+  const int lane = threadIdx.x & 31;
+  const int a0 = __ldg(p.item_ptr + v), a1 = __ldg(p.item_ptr + v + 1);
+  float fx = 0.f, fy = 0.f;
+  for (int a = a0 + lane; a < a1; a += 32) {
+    while (bl_ld_acquire(p.aflag + a) != stamp) __nanosleep(20);
+    const float2 q = __ldcg(p.attr + a);
+    fx += q.x;
+    fy += q.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+  }
+  return make_float2(fx, fy);
+}
+
+// Force of vertex v (one warp): CSR attraction + Barnes-Hut repulsion.
+// Returns the warp-summed force on every lane.
+__device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh, int v, float2 cv,
+                                                int plo, int phi, const float2 *pend,
+                                                unsigned stamp, unsigned long long &vis) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float fx = 0.f, fy = 0.f;
+  const bool split = __ldg(p.item_ptr + v + 1) - __ldg(p.item_ptr + v) > 1;
   // repulsion: frontier traversal from the root (Alg. S2)
   int *cur = sh.frontier[warp][0], *nxt = sh.frontier[warp][1];
   int ncur = 1;
@@ -506,15 +617,14 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
       const int idx = base + lane;
       const int k = idx < ncur ? cur[idx] : -1;
       int m = 0;
-      int4 kids = make_int4(-1, -1, -1, -1);
+      BHNode nd;
       if (k >= 0) {
-        const int4 B = __ldcg(p.nodeB + k);
+        nd = bh_load(p, k);
         ++vis;
-        if (B.x & (1 << 16)) {
-          bh_leaf_terms(p, B, v, cv.x, cv.y, fx, fy);
-        } else if (!bh_mac(p, __ldcg(p.nodeA + k), cv.x, cv.y, fx, fy)) {
-          m = (B.x >> 8) & 0xff;
-          kids = __ldcg(p.nodeC + k);
+        if (nd.B.x & (1 << 16)) {
+          bh_leaf_terms(p, nd, v, cv.x, cv.y, plo, phi, pend, fx, fy);
+        } else if (!bh_mac(p, nd.A, cv.x, cv.y, fx, fy)) {
+          m = (nd.B.x >> 8) & 0xff;
         }
       }
       int incl = m;
@@ -527,10 +637,12 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
       const bool fits = pos + m <= BH_FCAP;
       if (m > 0) {
         if (fits) {
-          const int ks[4] = {kids.x, kids.y, kids.z, kids.w};
-          for (int q = 0; q < m; ++q) nxt[pos + q] = ks[q];
+          nxt[pos] = k + 1;
+          if (m > 1) nxt[pos + 1] = nd.C.x;
+          if (m > 2) nxt[pos + 2] = nd.C.y;
+          if (m > 3) nxt[pos + 3] = nd.C.z;
         } else {
-          bh_walk_subtree(p, k, v, cv.x, cv.y, fx, fy, vis);  // frontier full
+          bh_walk_subtree(p, k, nd.B.w, v, cv.x, cv.y, plo, phi, pend, fx, fy, vis);  // full
         }
       }
       // entries written: the fitting lanes form a prefix of the warp
@@ -547,50 +659,85 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
     fx += __shfl_xor_sync(0xffffffffu, fx, o);
     fy += __shfl_xor_sync(0xffffffffu, fy, o);
   }
-  return make_float2(fx, fy);
+  // attraction f_a = d^2/K along the unit vector (Alg. S3 lines 15-17):
+  // inline for short rows, else the published item partials
+  const float2 fa = split ? bh_attr_gather(p, v, stamp)
+                          : bh_attr_range(p, __ldg(p.rowptr + v), __ldg(p.rowptr + v + 1), cv,
+                                          plo, phi, pend);
+  return make_float2(fx + fa.x, fy + fa.y);
 }
 
-// Alg. S3's iterations: tree per iteration, then the dependent minibatches.
+// Fixed-order sum of the G per-CTA fp64 energies by one warp (identical in
+// every CTA, so the tol decision is too).
+__device__ __forceinline__ double bh_energy_sum(const BHKParams &p) {
+  const int G = gridDim.x, lane = threadIdx.x & 31;
+  double e = 0.0;
+  for (int cc = lane; cc < G; cc += 32) e += __ldcg(p.e_cta + cc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  return e;
+}
+
+// Alg. S3's iterations: tree per iteration, then the dependent minibatches
+// with ONE grid barrier each.  Phase t: every warp computes the force of its
+// batch-t vertex and writes the new coordinate to pend[t & 1] (not to xy:
+// other warps still read batch t's frozen coordinates); meanwhile batch t-1's
+// new coordinates are committed from pend to xy, and readers take batch t-1
+// vertices from pend.  The last batch of an iteration is committed before the
+// next tree is built (its own barrier).
 template <int NT>
 __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_target,
-                               int *unit_dummy_ptr, unsigned long long &vis) {
+                               int *unit_dummy_ptr, unsigned long long &vis, BLProf &pf) {
   const int G = gridDim.x, c = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = c * BH_NW + warp, GW = G * BH_NW;
-  double step = p.step0, e_prev = 0.0, e_acc = 0.0;
+  double step = p.step0, e_prev = 0.0;
   int batches = 0, done = 0;
   bool stop = false;
+  int plo = 0, phi = 0;  // batch whose new coordinates are still in pend
   for (int it = 0; it < p.iters && !stop; ++it) {
-    bh_build_tree<NT>(p, sh, bar_target, unit_dummy_ptr);  // Alg. S3 lines 5-8
-    e_acc = 0.0;
+    if (phi > plo) {  // commit the previous iteration's last batch
+      const float2 *pd = p.pend + (size_t)(((batches - 1) & 1) * p.b);
+      for (int i = c * NT + threadIdx.x; i < phi - plo; i += G * NT) p.xy[plo + i] = __ldcg(pd + i);
+      plo = phi = 0;
+      bl_grid_sync(p.bar, bar_target, unit_dummy_ptr);
+    }
+    pf.mark(4);
+    bh_build_tree<NT>(p, sh, bar_target, unit_dummy_ptr, pf);  // Alg. S3 lines 5-8
+    double e_acc = 0.0;
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b, bt = min(p.b, p.n - lo);
-      // F: forces of the batch, coordinates frozen (lines 13-20)
+      float2 *pend_t = p.pend + (size_t)((batches & 1) * p.b);
+      const float2 *pend_prev = p.pend + (size_t)(((batches - 1) & 1) * p.b);
+      // commit batch t-1 (nobody reads its xy entries in this phase)
+      for (int i = c * NT + threadIdx.x; i < phi - plo; i += G * NT)
+        p.xy[plo + i] = __ldcg(pend_prev + i);
+      // F: forces of batch t against frozen coordinates (lines 13-20), then
+      // the update (lines 21-24) into pend.  Long CSR rows first, edge-
+      // parallel over all warps (no warp waits before its items are done).
+      const unsigned stamp = (unsigned)batches + 1u;
+      bh_attr_items(p, lo, lo + bt, gw, GW, stamp, plo, phi, pend_prev);
       for (int i = gw; i < bt; i += GW) {
-        const float2 f = bh_force_warp(p, sh, lo + i, vis);
-        if (lane == 0) p.fb[i] = f;
-      }
-      bl_grid_sync(p.bar, bar_target, unit_dummy_ptr);
-      // U: owner update (lines 21-24); CTA c owns batch entries c, c+G, ...
-      for (int i = c + G * threadIdx.x; i < bt; i += G * NT) {
-        const float2 f = __ldcg(p.fb + i);
-        const double q = (double)f.x * f.x + (double)f.y * f.y;
-        if (q > 0.0) {
-          const double s = step / sqrt(q);
-          float2 cv = __ldcg(p.xy + lo + i);
-          cv.x = (float)((double)cv.x + s * f.x);
-          cv.y = (float)((double)cv.y + s * f.y);
-          p.xy[lo + i] = cv;
+        const int v = lo + i;
+        const float2 cv = __ldcg(p.xy + v);
+        const float2 f = bh_force_warp(p, sh, v, cv, plo, phi, pend_prev, stamp, vis);
+        if (lane == 0) {
+          const double q = (double)f.x * f.x + (double)f.y * f.y;
+          float2 nv = cv;
+          if (q > 0.0) {
+            const double s = step / sqrt(q);
+            nv.x = (float)((double)cv.x + s * f.x);
+            nv.y = (float)((double)cv.y + s * f.y);
+          }
+          pend_t[i] = nv;
+          e_acc += q;
         }
-        e_acc += q;
       }
       ++batches;
       const bool last = t == p.nb - 1;
       const bool mb = p.max_batches > 0 && batches >= p.max_batches;
       if (last || mb) {
-        double e = e_acc;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        double e = e_acc;  // only lane 0 of each warp holds a value
         if (lane == 0) sh.e_warp[warp] = e;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -599,12 +746,14 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
           p.e_cta[c] = s;
         }
       }
+      pf.mark(5);
       bl_grid_sync(p.bar, bar_target, unit_dummy_ptr);
+      pf.mark(6);
+      plo = lo;
+      phi = lo + bt;
       if (last || mb) {
-        // every CTA sums the per-CTA energies in the same order, so the tol
-        // decision is identical everywhere
-        double E = 0.0;
-        for (int cc = 0; cc < G; ++cc) E += __ldcg(p.e_cta + cc);
+        // identical fixed-order sum in every CTA -> identical tol decision
+        const double E = bh_energy_sum(p);
         if (c == 0 && threadIdx.x == 0) p.energy[it] = E;
         if (mb) {
           stop = true;
@@ -620,6 +769,11 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
     }
     step = step * p.cooling;
   }
+  // commit the last batch (the kernel ends: no reader left)
+  if (phi > plo) {
+    const float2 *pd = p.pend + (size_t)(((batches - 1) & 1) * p.b);
+    for (int i = c * NT + threadIdx.x; i < phi - plo; i += G * NT) p.xy[plo + i] = __ldcg(pd + i);
+  }
   if (c == 0 && threadIdx.x == 0) *p.iters_done = done;
 }
 
@@ -634,15 +788,26 @@ __global__ void __launch_bounds__(NT, 1) bl_bh_kernel(BHKParams p) {
   unsigned bar_target = 0;
   unsigned long long vis = 0;
   const int gw = c * BH_NW + warp, GW = G * BH_NW;
+  BLProf pf;
+  pf.on = p.prof != nullptr && threadIdx.x == 0;
+  for (int i = 0; i < 8; ++i) pf.acc[i] = 0;
+  pf.last = pf.on ? clock64() : 0;
 
   if (p.forces_mode) {
-    bh_build_tree<NT>(p, sh, bar_target, &unit_dummy);
+    bh_build_tree<NT>(p, sh, bar_target, &unit_dummy, pf);
+    bh_attr_items(p, p.first, p.first + p.count, gw, GW, 1u, 0, 0, p.pend);
     for (int t = gw; t < p.count; t += GW) {
-      const float2 f = bh_force_warp(p, sh, p.first + t, vis);
+      const int v = p.first + t;
+      const float2 f = bh_force_warp(p, sh, v, __ldcg(p.xy + v), 0, 0, p.pend, 1u, vis);
       if (lane == 0) p.f_out[t] = f;
     }
   } else {
-    bh_run_batches<NT>(p, sh, bar_target, &unit_dummy, vis);
+    bh_run_batches<NT>(p, sh, bar_target, &unit_dummy, vis, pf);
+  }
+  if (pf.on) {
+    if (c == 0)
+      for (int i = 0; i < 8; ++i) p.prof[i] = pf.acc[i];
+    p.prof[8 + c] = pf.acc[5];
   }
 
   // visits: per-CTA totals (deterministic sum later on the host)
