@@ -114,6 +114,16 @@ bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p, void *cud
 bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t trace_len,
                     int32_t *n_written, int32_t *iters_done);
 
+/* Greedy initial layout, Alg. 3 (§3.6): host-only (needs
+ * no GPU and no context), O(n + m).  rowptr/colidx: CSR of G as for
+ * bl_create (only ranges are validated here); root: the start vertex V0
+ * (the paper picks it at random), placed at (0, 0); xy_out: 2n floats
+ * (caller-owned).  Components other than V0's restart from their smallest
+ * vertex id at origins on a square grid (reading G3).
+ * BL_EINVAL on bad arguments. */
+bl_status bl_greedy_init(int32_t n, const int32_t *rowptr, const int32_t *colidx, int32_t root,
+                         float *xy_out);
+
 /* Debug / parity: the raw combined forces f(i, c) of §2.2 for
  * i in [first, first+count) at the device state d_xy (not modified), written
  * to d_f_out (float2[count], device).  Uses the same device code as the

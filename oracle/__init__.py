@@ -22,6 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bl_oracle.c")
 _IMPL = os.path.join(_HERE, "bl_oracle_impl.h")
 _BH = os.path.join(_HERE, "bl_oracle_bh.h")
+_INIT = os.path.join(_HERE, "bl_oracle_init.h")
 _SO = os.path.join(_HERE, "libbl_oracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -31,7 +32,8 @@ REPULSE_NEIGHBORS = 1
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc: -O2 -ffp-contract=off, no fast-math."""
-    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_IMPL), os.path.getmtime(_BH))
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_IMPL), os.path.getmtime(_BH),
+                 os.path.getmtime(_INIT))
     if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= newest:
         return _SO
     tmp = _SO + f".tmp{os.getpid()}"
@@ -69,6 +71,8 @@ def _load():
         lib.oracle_bh_layout.restype = ctypes.c_int
         lib.oracle_bh_tree.argtypes = [i32, vp, i32] + [vp] * 10
         lib.oracle_bh_tree.restype = ctypes.c_int
+        lib.oracle_greedy_init.argtypes = [i32, vp, vp, i32, vp]
+        lib.oracle_greedy_init.restype = ctypes.c_int
         del ll
         _lib = lib
         return lib
@@ -199,4 +203,15 @@ def bh_tree(xy):
     out = {k: v[:nn] for k, v in a.items()}
     out.update(child=child[:4 * nn].reshape(nn, 4), cx=cx[:nn], cy=cy[:nn], codes=codes,
                perm=perm, D=float(D.value))
+    return out
+
+
+# ------------------------------------------------------------ greedy init
+def greedy_init(n, rowptr, colidx, root=0):
+    """Alg. 3 (greedy initialisation) with readings G1-G4; (n, 2) float32."""
+    lib = _load()
+    rowptr, colidx = _csr(rowptr, colidx)
+    out = np.zeros((n, 2), np.float32)
+    if lib.oracle_greedy_init(n, _ptr(rowptr), _ptr(colidx), int(root), _ptr(out)) != 0:
+        raise ValueError("oracle_greedy_init: invalid arguments")
     return out

@@ -47,6 +47,9 @@
 /* BatchLayoutBH (Alg. S1-S3), fp64 force terms, fp32 decisions */
 #include "bl_oracle_bh.h"
 
+/* Greedy initialisation (Alg. 3) */
+#include "bl_oracle_init.h"
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -62,6 +62,8 @@ def _load() -> ctypes.CDLL:
     lib.bl_max_vertices.restype = i32
     lib.bl_last_launch_count.argtypes = [vp]
     lib.bl_last_launch_count.restype = i32
+    lib.bl_greedy_init.argtypes = [i32, vp, vp, i32, vp]
+    lib.bl_greedy_init.restype = ctypes.c_int
     lib.bl_last_visits.argtypes = [vp, P(ctypes.c_ulonglong)]
     lib.bl_last_visits.restype = ctypes.c_int
     lib.bl_kernel_name.argtypes = [vp]
@@ -82,7 +84,7 @@ def _load() -> ctypes.CDLL:
 lib = _load()
 
 # symbols include/bl.h declares (checked by tests/test_abi.py)
-EXPORTS = ("bl_params_default", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
+EXPORTS = ("bl_params_default", "bl_greedy_init", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
            "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_microbench",
            "bl_debug_profile", "bl_destroy", "bl_status_string", "bl_last_error")
 
@@ -167,6 +169,18 @@ def bl_max_vertices() -> int:
 
 def bl_last_launch_count(h: int) -> int:
     return int(lib.bl_last_launch_count(h))
+
+
+def bl_greedy_init(n: int, rowptr, colidx, root: int = 0) -> np.ndarray:
+    """Alg. 3 greedy initial layout (host C++ in libbl); (n, 2) float32."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int32)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    out = np.zeros((int(n), 2), dtype=np.float32)
+    rc = lib.bl_greedy_init(int(n), rowptr.ctypes.data, colidx.ctypes.data if colidx.size else 0,
+                            int(root), out.ctypes.data)
+    if rc != BL_OK:
+        raise BLError(rc, f"{lib.bl_status_string(rc).decode()}: bl_greedy_init")
+    return out
 
 
 def bl_last_visits(h: int) -> int:

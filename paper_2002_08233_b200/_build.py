@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbl.so")
-SOURCES = ["bl_api.cu", "bl_microbench.cu"]
+SOURCES = ["bl_api.cu", "bl_microbench.cu", "bl_init.cu"]
 HEADERS = ["bl_kernel.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
