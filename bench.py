@@ -227,7 +227,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     params = dict(iters=cfg.iters, batch=cfg.batch, K=cfg.K, C=cfg.C, step0=cfg.step0,
-                  cooling=cfg.cooling)
+                  cooling=cfg.cooling, a=args.a, r=args.r)
     lay = bl.BatchLayout(g.n, g.rowptr, g.colidx)
     d_xy0 = torch.from_numpy(xy0.copy()).to(dev)
     d_xy = torch.empty_like(d_xy0)
@@ -282,7 +282,8 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     clocks = clk.summary()
     sm_max = float(clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = nsm * MUFU_PER_CLK_SM * sm_max * 1e6
+    mufu_per_pair = 1 if args.r == -1.0 else 2   # r != -1: lg2 + ex2
+    peak = nsm * MUFU_PER_CLK_SM * sm_max * 1e6 / mufu_per_pair
     achieved = pairs_per_step / (t_local / args.steps)
     kname = bl.bl_kernel_name(lay.h)
     traffic, traffic_src = load_traffic(name, kname)
@@ -290,7 +291,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(workload_desc(name, g, cfg),
+        "config": dict(workload_desc(name, g, cfg), model={"a": args.a, "r": args.r},
                        l2="flushed (512 MiB write) before every timed step",
                        parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
         "iters_per_sec": world * args.steps * cfg.iters / t_max,
@@ -300,9 +301,10 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
             "traffic_source": traffic_src,
             "kernel": kname + " (persistent, cooperative; NT threads, T targets/thread, TP of them "
                               "paired-reciprocal)",
-            "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU.RCP/clk x {sm_max:.0f} MHz "
-                          f"(sm_max_mhz, {peak_src}); 1 MUFU per pair",
-            "frac_at_median_clock": (achieved / (nsm * MUFU_PER_CLK_SM * clocks["sm_mhz"] * 1e6)
+            "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU/clk x {sm_max:.0f} MHz "
+                          f"(sm_max_mhz, {peak_src}) / {mufu_per_pair} MUFU per pair",
+            "frac_at_median_clock": (achieved * mufu_per_pair
+                                     / (nsm * MUFU_PER_CLK_SM * clocks["sm_mhz"] * 1e6)
                                      if clocks.get("sm_mhz") else None),
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * g.n,
@@ -399,6 +401,8 @@ def main(argv=None):
     ap.add_argument("--prof", action="store_true", help="add a phase profile (extra untimed run)")
     ap.add_argument("--no-bh", action="store_true", help="skip the secondary BatchLayoutBH line")
     ap.add_argument("--theta", type=float, default=1.2, help="BatchLayoutBH MAC threshold (P:869)")
+    ap.add_argument("--a", type=float, default=2.0, help="(a, r)-model attraction exponent (P:531)")
+    ap.add_argument("--r", type=float, default=-1.0, help="(a, r)-model repulsion exponent")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -72,11 +72,18 @@ typedef struct {
   float theta;         /* BL_ALGO_BH: MAC threshold, accept a cell when
                           theta > D_cell / d; >= 0, 0 = exact; the
                           paper's value 1.2 is the default             */
+  float a;             /* (a, r)-energy model (§2.2, reading C15): the
+                          attractive force is d^a / K, a in [0, 4]; 2 = the
+                          paper's model, 1 = ForceAtlas2, 0 = LinLog  */
+  float r;             /* the repulsive force magnitude is C K^2 d^r, r in
+                          [-3, 1); -1 = the paper's (Fruchterman-Reingold).
+                          r != -1 costs two SFU ops per pair instead of one    */
 } bl_params;
 
 /* Fill p with the paper's defaults: iters 600 (the CLI default),
  * batch 256, K = 1, C = 1, step0 = 1.0, cooling = 0.999, tol = 0,
- * max_batches = 0, flags = 0, algo = BL_ALGO_EXACT, theta = 1.2. */
+ * max_batches = 0, flags = 0, algo = BL_ALGO_EXACT, theta = 1.2,
+ * a = 2, r = -1. */
 void bl_params_default(bl_params *p);
 
 /* Create a context on the current CUDA device for the undirected graph G

@@ -71,11 +71,28 @@ def _load():
         lib.oracle_bh_layout.restype = ctypes.c_int
         lib.oracle_bh_tree.argtypes = [i32, vp, i32] + [vp] * 10
         lib.oracle_bh_tree.restype = ctypes.c_int
+        lib.oracle_set_model.argtypes = [dbl, dbl]
+        lib.oracle_set_model.restype = None
         lib.oracle_greedy_init.argtypes = [i32, vp, vp, i32, vp]
         lib.oracle_greedy_init.restype = ctypes.c_int
         del ll
         _lib = lib
         return lib
+
+
+class _model:
+    """Set the (a, r)-energy model exponents for one call (reading C15)."""
+
+    def __init__(self, a, r):
+        self.a, self.r = float(a), float(r)
+
+    def __enter__(self):
+        _lock.acquire()
+        _lib.oracle_set_model(self.a, self.r)
+
+    def __exit__(self, *exc):
+        _lib.oracle_set_model(2.0, -1.0)
+        _lock.release()
 
 
 def _ptr(a: np.ndarray):
@@ -95,7 +112,8 @@ def max_threads() -> int:
 
 
 def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
-           cooling=0.999, max_batches=0, tol=0.0, flags=0, threads=0, precision="f64"):
+           cooling=0.999, max_batches=0, tol=0.0, flags=0, threads=0, precision="f64",
+           a=2.0, r=-1.0):
     """Run Alg. 2 from xy0 ((n,2) any float dtype; converted to the oracle's
     precision).  Returns (xy (n,2), energy[iters] fp64, iters_done)."""
     lib = _load()
@@ -105,15 +123,16 @@ def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
     energy = np.zeros(max(iters, 1), dtype=np.float64)
     done = ctypes.c_int32(0)
     fn = getattr(lib, f"oracle_layout_{precision}")
-    rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0, cooling,
-            max_batches, tol, flags, _ptr(energy), ctypes.byref(done), threads)
+    with _model(a, r):
+        rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0, cooling,
+                max_batches, tol, flags, _ptr(energy), ctypes.byref(done), threads)
     if rc != 0:
         raise ValueError("oracle_layout: invalid arguments")
     return xy, energy[:int(done.value) if tol > 0 else iters], int(done.value)
 
 
 def forces(n, rowptr, colidx, xy, first=0, count=None, *, K=1.0, C=1.0, flags=0,
-           threads=0, precision="f64"):
+           threads=0, precision="f64", a=2.0, r=-1.0):
     """f(i, c) of §2.2 for i in [first, first+count) at state xy; (count, 2)."""
     lib = _load()
     if count is None:
@@ -123,7 +142,9 @@ def forces(n, rowptr, colidx, xy, first=0, count=None, *, K=1.0, C=1.0, flags=0,
     rowptr, colidx = _csr(rowptr, colidx)
     out = np.zeros((max(count, 1), 2), dtype=dt)
     fn = getattr(lib, f"oracle_forces_{precision}")
-    rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(c), first, count, K, C, flags, _ptr(out), threads)
+    with _model(a, r):
+        rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(c), first, count, K, C, flags, _ptr(out),
+                threads)
     if rc != 0:
         raise ValueError("oracle_forces: invalid arguments")
     return out[:count]
@@ -144,7 +165,7 @@ THETA_PAPER = 1.2  # MAC threshold
 
 
 def bh_layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0, cooling=0.999,
-              theta=THETA_PAPER, max_batches=0, tol=0.0):
+              theta=THETA_PAPER, max_batches=0, tol=0.0, a=2.0, r=-1.0):
     """Alg. S3 (BatchLayoutBH) from xy0.  Returns (xy (n,2) fp64, energy,
     iters_done, node visits)."""
     lib = _load()
@@ -153,16 +174,17 @@ def bh_layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0, 
     energy = np.zeros(max(iters, 1), dtype=np.float64)
     done = ctypes.c_int32(0)
     visits = ctypes.c_longlong(0)
-    rc = lib.oracle_bh_layout(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0,
-                              cooling, theta, max_batches, tol, _ptr(energy), ctypes.byref(done),
-                              ctypes.byref(visits))
+    with _model(a, r):
+        rc = lib.oracle_bh_layout(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C,
+                                  step0, cooling, theta, max_batches, tol, _ptr(energy),
+                                  ctypes.byref(done), ctypes.byref(visits))
     if rc != 0:
         raise ValueError("oracle_bh_layout: invalid arguments")
     return xy, energy[:int(done.value) if tol > 0 else iters], int(done.value), int(visits.value)
 
 
 def bh_forces(n, rowptr, colidx, snap, live, first=0, count=None, *, K=1.0, C=1.0,
-              theta=THETA_PAPER):
+              theta=THETA_PAPER, a=2.0, r=-1.0):
     """Forces of Alg. S3 lines 13-19 for [first, first+count): tree built from
     `snap` (rounded to fp32), live coordinates `live`.  Returns ((count,2)
     fp64, node visits)."""
@@ -174,8 +196,9 @@ def bh_forces(n, rowptr, colidx, snap, live, first=0, count=None, *, K=1.0, C=1.
     rowptr, colidx = _csr(rowptr, colidx)
     out = np.zeros((max(count, 1), 2), dtype=np.float64)
     visits = ctypes.c_longlong(0)
-    rc = lib.oracle_bh_forces(n, _ptr(rowptr), _ptr(colidx), _ptr(s), _ptr(c), first, count, K, C,
-                              theta, _ptr(out), ctypes.byref(visits))
+    with _model(a, r):
+        rc = lib.oracle_bh_forces(n, _ptr(rowptr), _ptr(colidx), _ptr(s), _ptr(c), first, count,
+                                  K, C, theta, _ptr(out), ctypes.byref(visits))
     if rc != 0:
         raise ValueError("oracle_bh_forces: invalid arguments")
     return out[:count], int(visits.value)

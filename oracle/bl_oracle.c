@@ -28,21 +28,35 @@
 #include <omp.h>
 #endif
 
+/* (a, r)-energy model exponents (§2.2, reading C15 of
+ * DESIGN.md §3): attraction magnitude d^a / K, repulsion magnitude C K^2 d^r
+ * (Noack / ForceAtlas2 convention: (2,-1) = Fruchterman-Reingold).
+ * Process-global, set by the Python face around each call. */
+static double g_model_a = 2.0, g_model_r = -1.0;
+void oracle_set_model(double a, double r) {
+  g_model_a = a;
+  g_model_r = r;
+}
+
 #define REAL double
 #define SFX(name) name##_f64
 #define SQRT sqrt
+#define POW pow
 #include "bl_oracle_impl.h"
 #undef REAL
 #undef SFX
 #undef SQRT
+#undef POW
 
 #define REAL float
 #define SFX(name) name##_f32
 #define SQRT sqrtf
+#define POW powf
 #include "bl_oracle_impl.h"
 #undef REAL
 #undef SFX
 #undef SQRT
+#undef POW
 
 /* BatchLayoutBH (Alg. S1-S3), fp64 force terms, fp32 decisions */
 #include "bl_oracle_bh.h"

@@ -199,8 +199,14 @@ static void bh_repulse(const bh_tree *t, int r, int32_t i, double xi, double yi,
       const double dx = c[2 * j] - xi, dy = c[2 * j + 1] - yi;
       const double d2 = dx * dx + dy * dy;
       if (d2 == 0) continue;
-      *fx = *fx - ck2 * dx / d2; /* f_r(d) * (c_j - c_i)/d, f_r = -CK^2/d */
-      *fy = *fy - ck2 * dy / d2;
+      if (g_model_r == -1.0) {
+        *fx = *fx - ck2 * dx / d2; /* f_r(d) * (c_j - c_i)/d, f_r = -CK^2/d */
+        *fy = *fy - ck2 * dy / d2;
+      } else {
+        const double d = sqrt(d2), w = ck2 * pow(d, g_model_r) / d; /* f_r = -CK^2 d^r */
+        *fx = *fx - w * dx;
+        *fy = *fy - w * dy;
+      }
     }
     return;
   }
@@ -214,8 +220,14 @@ static void bh_repulse(const bh_tree *t, int r, int32_t i, double xi, double yi,
     const double dx = (double)nd->cx - xi, dy = (double)nd->cy - yi;
     const double d2 = dx * dx + dy * dy;
     if (d2 > 0) {
-      *fx = *fx - (double)nd->count * ck2 * dx / d2;
-      *fy = *fy - (double)nd->count * ck2 * dy / d2;
+      if (g_model_r == -1.0) {
+        *fx = *fx - (double)nd->count * ck2 * dx / d2;
+        *fy = *fy - (double)nd->count * ck2 * dy / d2;
+      } else {
+        const double d = sqrt(d2), w = (double)nd->count * ck2 * pow(d, g_model_r) / d;
+        *fx = *fx - w * dx;
+        *fy = *fy - w * dy;
+      }
     }
     return;
   }
@@ -236,7 +248,7 @@ static void bh_force(int32_t n, const int32_t *rowptr, const int32_t *colidx, co
     const double dx = c[2 * j] - xi, dy = c[2 * j + 1] - yi;
     const double d = sqrt(dx * dx + dy * dy);
     if (d == 0) continue;
-    const double fa = d * d / K; /* f_a = ||c_i - c_j||^2 / K */
+    const double fa = f_attr_f64(d, K); /* f_a = ||c_i - c_j||^a / K */
     fx = fx + fa * dx / d;
     fy = fy + fa * dy / d;
   }

@@ -7,15 +7,22 @@
  * Requires: REAL, SFX(name), SQRT defined by the includer.
  */
 
-/* f_a(i,j) = ||c_i - c_j||^a / K with a = 2  (§2.2, P:524-528;
- * (a, r) = (2, -1) is the paper's evaluated model). */
-static REAL SFX(f_attr)(REAL d, REAL K) { return (d * d) / K; }
+/* f_a(i,j) = ||c_i - c_j||^a / K  (§2.2); a = 2 is the
+ * paper's evaluated model (2,-1); other a: the (a,r)-energy model
+ * family, exponent set by oracle_set_model (reading C15). */
+static REAL SFX(f_attr)(REAL d, REAL K) {
+  if (g_model_a == 2.0) return (d * d) / K;
+  return POW(d, (REAL)g_model_a) / K;
+}
 
 /* f_r(i,j) = -R K^2 / ||c_i - c_j|| (§2.2, under the
  * reading C1 of DESIGN.md: the (2,-1) model's repulsive force magnitude is
  * R K^2 / d, i.e. the Fruchterman-Reingold repulsion P:872).  R is called
  * C here (Hu's notation). */
-static REAL SFX(f_rep)(REAL d, REAL K, REAL C) { return -(C * K * K) / d; }
+static REAL SFX(f_rep)(REAL d, REAL K, REAL C) {
+  if (g_model_r == -1.0) return -(C * K * K) / d;
+  return -(C * K * K) * POW(d, (REAL)g_model_r); /* magnitude C K^2 d^r (C15) */
+}
 
 /* Force of vertex i against the frozen coordinates c, exactly as the inner
  * loops of Alg. 1 / Alg. 2: for every j != i, if

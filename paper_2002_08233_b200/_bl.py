@@ -30,6 +30,8 @@ class bl_params(ctypes.Structure):
         ("flags", ctypes.c_uint32),
         ("algo", ctypes.c_int32),
         ("theta", ctypes.c_float),
+        ("a", ctypes.c_float),
+        ("r", ctypes.c_float),
     ]
 
 

@@ -116,6 +116,16 @@ extern "C" void bl_params_default(bl_params *p) {
   p->flags = 0;
   p->algo = BL_ALGO_EXACT;
   p->theta = 1.2f;
+  p->a = 2.0f;
+  p->r = -1.0f;
+}
+
+// (a, r)-energy model codes shared by both kernels (reading C15)
+static void model_codes(const bl_params *p, int *amode, int *rmode, float *a_half, float *r_half) {
+  *amode = p->a == 2.0f ? 0 : p->a == 1.0f ? 1 : p->a == 0.0f ? 2 : p->a == 3.0f ? 3 : 4;
+  *rmode = p->r == -1.0f ? 0 : 1;
+  *a_half = 0.5f * (p->a - 1.0f);
+  *r_half = 0.5f * (p->r - 1.0f);
 }
 
 extern "C" const char *bl_status_string(bl_status s) {
@@ -179,6 +189,7 @@ static const BLVariant kVariants[] = {
     BL_V(512, 8, 2),  BL_V(512, 8, 3),  BL_V(512, 8, 4),  BL_V(512, 4, 2),
     BL_V(768, 6, 2),  BL_V(768, 4, 1),  BL_V(768, 4, 2),
     BL_V(1024, 4, 1), BL_V(1024, 4, 2), BL_V(1024, 2, 1),
+    BL_V(512, 8, -1),  // general repulsion exponent r (reading C15)
 };
 #undef BL_V
 static const BLVariant *find_variant(int NT, int T, int TP) {
@@ -352,6 +363,8 @@ static bl_status check_params(bl_ctx *h, const bl_params *p) {
   if (p->algo != BL_ALGO_EXACT && p->algo != BL_ALGO_BH) return fail(h, BL_EINVAL, "unknown algo");
   if (p->algo == BL_ALGO_BH && (!(p->theta >= 0.f) || !std::isfinite(p->theta)))
     return fail(h, BL_EINVAL, "theta must be >= 0");
+  if (!(p->a >= 0.f && p->a <= 4.f)) return fail(h, BL_EINVAL, "a must be in [0, 4]");
+  if (!(p->r >= -3.f && p->r < 1.f)) return fail(h, BL_EINVAL, "r must be in [-3, 1)");
   return BL_OK;
 }
 
@@ -436,8 +449,9 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
 
   k.red_cap = red_cap_for(k.chunk4);
   k.guided = env_int("BL_GUIDED", 2);
+  model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
-  const BLVariant *vt = find_variant(h->NT, h->T, h->TP);
+  const BLVariant *vt = k.rmode == 0 ? find_variant(h->NT, h->T, h->TP) : find_variant(512, 8, -1);
   void *kfn = vt->fn;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
@@ -504,6 +518,7 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.invK = 1.0f / p->K;
   const float th = p->theta;
   k.theta2 = th * th;  // fp32, as the oracle (reading B7)
+  model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
   k.step0 = p->step0;
   k.cooling = p->cooling;
   k.tol = p->tol;

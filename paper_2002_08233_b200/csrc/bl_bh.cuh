@@ -39,6 +39,8 @@
 struct BHKParams {
   int n, b, nb, iters, max_batches;
   float ck2, invK, theta2;
+  int amode, rmode;       // (a, r)-energy model, as BLKParams (reading C15)
+  float a_half, r_half;
   double step0, cooling, tol;
   int forces_mode, first, count;
   float2 *xy;
@@ -481,6 +483,11 @@ __device__ __forceinline__ float2 bh_live(const BHKParams &p, int j, int plo, in
   return (j >= plo && j < phi) ? __ldcg(pend + (j - plo)) : __ldcg(p.xy + j);
 }
 
+// Repulsion weight of Δ at squared distance d2: C K^2 d^(r-1) (reading C15)
+__device__ __forceinline__ float bh_rep_weight(const BHKParams &p, float d2) {
+  return p.rmode == 0 ? p.ck2 / d2 : p.ck2 * bl_pow_d2(d2, p.r_half);
+}
+
 // Exact repulsive terms of a leaf's vertices against vertex v at (qx, qy)
 // (readings B5/B8/B9).
 __device__ __forceinline__ void bh_leaf_terms(const BHKParams &p, const BHNode &nd, int v, float qx,
@@ -494,7 +501,7 @@ __device__ __forceinline__ void bh_leaf_terms(const BHKParams &p, const BHNode &
     const float dx = cj.x - qx, dy = cj.y - qy;
     const float d2 = fmaf(dx, dx, dy * dy);
     if (d2 > 0.f) {
-      const float r = p.ck2 / d2;
+      const float r = bh_rep_weight(p, d2);
       fx = fmaf(-r, dx, fx);
       fy = fmaf(-r, dy, fy);
     }
@@ -508,7 +515,7 @@ __device__ __forceinline__ bool bh_mac(const BHKParams &p, const float4 &A, floa
   const float dx = __fsub_rn(A.x, qx), dy = __fsub_rn(A.y, qy);
   const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
   if (!(__fmul_rn(p.theta2, d2) > A.z)) return false;
-  const float r = A.w * p.ck2 / d2;
+  const float r = A.w * bh_rep_weight(p, d2);
   fx = fmaf(-r, dx, fx);
   fy = fmaf(-r, dy, fy);
   return true;
@@ -546,9 +553,16 @@ __device__ __forceinline__ float2 bh_attr_range(const BHKParams &p, int k0, int 
     const float dx = cj.x - cv.x, dy = cj.y - cv.y;
     const float d2 = fmaf(dx, dx, dy * dy);
     if (d2 > 0.f) {
-      const float d = sqrtf(d2);
-      fx = fmaf(d * p.invK, dx, fx);
-      fy = fmaf(d * p.invK, dy, fy);
+      float at;  // f_a(d)/d = d^(a-1)/K
+      switch (p.amode) {
+        case 0: at = sqrtf(d2); break;
+        case 1: at = 1.f; break;
+        case 2: at = rsqrtf(d2); break;
+        case 3: at = d2; break;
+        default: at = bl_pow_d2(d2, p.a_half);
+      }
+      fx = fmaf(at * p.invK, dx, fx);
+      fy = fmaf(at * p.invK, dy, fy);
     }
   }
 #pragma unroll

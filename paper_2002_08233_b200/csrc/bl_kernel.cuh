@@ -99,6 +99,10 @@ struct BLKParams {
   int chunk4;            // float4 slots (2 sources each) per CTA chunk
   int red_cap;           // float2 slots of the shared partial buffer
   int guided;            // sub-range size profile (bl_guided_start)
+  // (a, r)-energy model (reading C15): attraction d^a/K, repulsion C K^2 d^r;
+  // amode 0..3: a = 2, 1, 0, 3 (no pow), 4: general; rmode 0: r = -1, 1: general
+  int amode, rmode;
+  float a_half, r_half;  // (a-1)/2, (r-1)/2: vector coefficients d^(a-1), d^(r-1)
   int forces_mode, first, count;
   float2 *xy;
   const int *rowptr, *colidx;
@@ -122,6 +126,18 @@ __device__ __forceinline__ float bl_rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+__device__ __forceinline__ float bl_ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float bl_lg2(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// d^(2h) from d^2 on the SFU (two MUFU): the general (a, r)-model powers
+__device__ __forceinline__ float bl_pow_d2(float d2, float h) { return bl_ex2(h * bl_lg2(d2)); }
 __device__ __forceinline__ float bl_rsqrt(float x) {
   float r;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -177,10 +193,12 @@ __device__ __forceinline__ float2 bl_src_get(const float4 *src4, int k) {
 // for real sources (d^2 >= 2^-63 by the eps fold, so d2a d2b >= 2^-126;
 // d^2 < 1.8e19); dummy (far)
 // sources are only ever swept with TP = 0.
+// TP < 0: the general repulsion exponent r: INV = d^(r-1) = 2^(rh lg2 d^2)
+// (two MUFU per pair: the roofline halves).
 template <int T, int TP>
 __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0, int s1,
                                          const float (&tx)[T], const float (&ty)[T], bl_f2 (&AX)[T],
-                                         bl_f2 (&AY)[T]) {
+                                         bl_f2 (&AY)[T], float rh = 0.f) {
   const bl_f2 EPS = f2pack(BL_EPS2, BL_EPS2);
   bl_f2 TX[T], TY[T];
 #pragma unroll
@@ -200,7 +218,9 @@ __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0
       float a, b;
       f2unpack(D2, a, b);
       bl_f2 INV;
-      if (k < TP) {
+      if (TP < 0) {
+        INV = f2pack(bl_pow_d2(a, rh), bl_pow_d2(b, rh));
+      } else if (k < TP) {
         const float r = bl_rcp(a * b);
         INV = f2mul(f2pack(b, a), f2pack(r, r));
       } else {
@@ -210,6 +230,23 @@ __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0
       AY[k] = f2fma(DY, INV, AY[k]);
     }
   }
+}
+
+// Coefficient of Δ for one CSR neighbour (reading C15): attraction
+// f_a(d)/d = d^(a-1)/K plus, in the if/else model, the removal of the
+// all-pairs repulsion rep * d^(r-1) (rep = C K^2, or 0 with
+// BL_REPULSE_NEIGHBORS).  rs = 1/d.
+__device__ __forceinline__ float bl_model_coef(const BLKParams &p, float d2, float rs, float rep) {
+  float at;
+  switch (p.amode) {
+    case 0: at = d2 * rs; break;  // a = 2 (the paper's FR model)
+    case 1: at = 1.f; break;      // a = 1
+    case 2: at = rs; break;       // a = 0
+    case 3: at = d2; break;       // a = 3
+    default: at = bl_pow_d2(d2, p.a_half);
+  }
+  const float rv = p.rmode == 0 ? rs * rs : bl_pow_d2(d2, p.r_half);
+  return fmaf(rep, rv, at * p.invK);
 }
 
 __device__ __forceinline__ unsigned bl_ld_acquire(const unsigned *p) {
@@ -277,10 +314,11 @@ struct BLProf {
 template <int T, int TP>
 __device__ __forceinline__ void bl_sweep_range(const float4 *src4, int s0, int s1, int full4,
                                                const float (&tx)[T], const float (&ty)[T],
-                                               bl_f2 (&AX)[T], bl_f2 (&AY)[T]) {
+                                               bl_f2 (&AX)[T], bl_f2 (&AY)[T], float rh) {
+  constexpr int TP1 = TP < 0 ? TP : 0;  // the dummy-holding slot is never paired
   const int e = s1 < full4 ? s1 : full4;
-  if (s0 < e) bl_sweep<T, TP>(src4, s0, e, tx, ty, AX, AY);
-  if (s1 > full4 && s0 <= full4) bl_sweep<T, 0>(src4, full4, full4 + 1, tx, ty, AX, AY);
+  if (s0 < e) bl_sweep<T, TP>(src4, s0, e, tx, ty, AX, AY, rh);
+  if (s1 > full4 && s0 <= full4) bl_sweep<T, TP1>(src4, full4, full4 + 1, tx, ty, AX, AY, rh);
 }
 
 // Geometry of CTA c's resident sources: m_c = ceil((n - c)/G) owned
@@ -335,11 +373,12 @@ __device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, c
   if (sub < U.nc) {
     const int a = bl_guided_start(sub, U.nc, geo.clean4, p.guided);
     const int e = bl_guided_start(sub + 1, U.nc, geo.clean4, p.guided);
-    if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY);
+    if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY, p.r_half);
     if (e > geo.d_lo)
-      bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY);
+      bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY,
+                            p.r_half);
   } else {
-    bl_sweep_range<T, TP>(src4, geo.d_lo, geo.d_hi, geo.full4, tx, ty, AX, AY);
+    bl_sweep_range<T, TP>(src4, geo.d_lo, geo.d_hi, geo.full4, tx, ty, AX, AY, p.r_half);
   }
 #pragma unroll
   for (int k = 0; k < T; ++k) {
@@ -430,8 +469,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
         const float dx = cj.x - ci.x, dy = cj.y - ci.y;
         const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
         const float rs = bl_rsqrt(d2);
-        const float d = d2 * rs;
-        const float coef = fmaf(rep * rs, rs, d * p.invK);
+        const float coef = bl_model_coef(p, d2, rs, rep);
         sx = fmaf(coef, dx, sx);
         sy = fmaf(coef, dy, sy);
       }
@@ -621,8 +659,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     const float dx = cj.x - ci.x, dy = cj.y - ci.y;
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
     const float rs = bl_rsqrt(d2);
-    const float d = d2 * rs;
-    const float coef = fmaf(rep * rs, rs, d * p.invK);
+    const float coef = bl_model_coef(p, d2, rs, rep);
     sx = fmaf(coef, dx, sx);
     sy = fmaf(coef, dy, sy);
   }

@@ -21,7 +21,7 @@ def dense_adj(n, rowptr, colidx):
     return A
 
 
-def _force(n, A, c, i, K, R, repulse_neighbors=False):
+def _force(n, A, c, i, K, R, repulse_neighbors=False, a=2.0, r=-1.0):
     fx = fy = 0.0
     for j in range(n):
         if j == i:
@@ -31,9 +31,9 @@ def _force(n, A, c, i, K, R, repulse_neighbors=False):
             continue
         ux = (c[j][0] - c[i][0]) / dist
         uy = (c[j][1] - c[i][1]) / dist
-        rep = -R * K * K / dist
+        rep = -R * K * K * math.pow(dist, r)     # (a, r)-model, reading C15
         if A[i][j]:
-            att = dist ** 2 / K
+            att = math.pow(dist, a) / K
             fx += att * ux
             fy += att * uy
             if repulse_neighbors:
@@ -65,7 +65,7 @@ def alg1(n, A, c0, iters, K=1.0, R=1.0, step0=1.0, factor=0.999):
 
 
 def alg2(n, A, c0, iters, BS, K=1.0, R=1.0, step0=1.0, factor=0.999,
-         repulse_neighbors=False):
+         repulse_neighbors=False, a=2.0, r=-1.0):
     """Algorithm 2 semantics: consecutive minibatches, forces of
     a batch against frozen coordinates, then the batch update."""
     c = [[float(p[0]), float(p[1])] for p in c0]
@@ -76,7 +76,7 @@ def alg2(n, A, c0, iters, BS, K=1.0, R=1.0, step0=1.0, factor=0.999,
         energy = 0.0
         for lo in range(0, n, BS):
             batch = range(lo, min(lo + BS, n))
-            ct = [_force(n, A, c, i, K, R, repulse_neighbors) for i in batch]
+            ct = [_force(n, A, c, i, K, R, repulse_neighbors, a, r) for i in batch]
             for i, (fx, fy) in zip(batch, ct):
                 norm = math.hypot(fx, fy)
                 if norm > 0:

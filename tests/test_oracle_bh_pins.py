@@ -208,3 +208,32 @@ def test_one_batch_leaves_the_rest_unchanged_and_tree_is_per_iteration():
     step = 0.999
     want = it1 + step * f / np.hypot(*f.T)[:, None]
     np.testing.assert_allclose(it2, want, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("ar", [(1.0, -1.0), (0.0, -1.0), (2.0, -2.0), (1.5, -0.5)])
+def test_theta_zero_exact_for_general_models(ar):
+    """Reading C15 in the BH oracle: theta = 0 equals the exact method with
+    neighbour repulsion for the (a, r) models too."""
+    a, r = ar
+    g = rmat_graph(7, 4, 0.57, 0.19, 0.19, seed=5)
+    xy0 = uniform_coords(g.n, 7)
+    bh, Eb, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=2, batch=32, theta=0.0,
+                                    a=a, r=r)
+    ex, Ee, _ = oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=2, batch=32,
+                              flags=oracle.REPULSE_NEIGHBORS, a=a, r=r)
+    assert np.abs(bh - ex).max() <= 1e-10 * np.ptp(ex, axis=0).max()
+    np.testing.assert_allclose(Eb, Ee, rtol=1e-10)
+
+
+def test_far_cluster_general_model():
+    """Far-cluster closed form with r = -2: -4 C K^2 d^(r-1) (r_c - q)."""
+    pts = np.array([[0.0, 0.0], [100.0, 0.3], [100.3, -0.3], [99.9, 0.1], [100.2, 0.0]],
+                   np.float32)
+    g = edges_to_csr(5, np.array([], np.int64), np.array([], np.int64))
+    f, _ = oracle.bh_forces(5, g.rowptr, g.colidx, pts, pts, 0, 1, K=1.0, C=2.0, theta=1.2,
+                            r=-2.0)
+    rc = np.array([np.float32(pts[1:, 0].astype(np.float64).mean()),
+                   np.float32(pts[1:, 1].astype(np.float64).mean())], np.float64)
+    d = rc - pts[0]
+    dist = np.hypot(*d)
+    np.testing.assert_allclose(f[0], -4 * 2.0 * dist ** (-3) * d, rtol=1e-12)

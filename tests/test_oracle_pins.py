@@ -401,3 +401,58 @@ def test_f32_variant_tracks_f64_for_one_iteration():
     ext = np.ptp(a, axis=0).max()
     assert np.abs(a - b).max() < 1e-4 * ext
     assert abs(Ea[0] - Eb[0]) < 1e-3 * Ea[0]
+
+
+# ------------------------------------------------------------ (a, r)-energy models (C15)
+
+@pytest.mark.parametrize("row", _golden("pairm"))
+def test_model_pair_force_worked_examples(row):
+    """(a, r)-energy model (§2.2): hand-derived pair forces."""
+    (adj, a, r, K, C, xi, yi, xj, yj), (fx, fy) = row
+    rp, ci = _edge_csr(2, [(0, 1)] if adj else [])
+    f = oracle.forces(2, rp, ci, np.array([[xi, yi], [xj, yj]]), 0, 1, K=K, C=C, a=a, r=r)
+    assert f[0, 0] == pytest.approx(fx, abs=1e-14)
+    assert f[0, 1] == pytest.approx(fy, abs=1e-14)
+
+
+@pytest.mark.parametrize("ar", [(1.0, -1.0), (0.0, -1.0), (3.0, -1.0), (2.0, -2.0),
+                                (1.5, -0.5)])
+@pytest.mark.parametrize("flags", [0, oracle.REPULSE_NEIGHBORS])
+def test_models_vs_bruteforce(ar, flags):
+    a, r = ar
+    rng = np.random.default_rng(int(10 * a - 7 * r) + flags)
+    for trial in range(6):
+        n = int(rng.integers(4, 8))
+        edges = [(i, j) for i in range(n) for j in range(i + 1, n) if rng.random() < 0.4]
+        rp, ci = _edge_csr(n, edges)
+        A = bruteforce.dense_adj(n, rp, ci)
+        xy0 = rng.random((n, 2)) * 3
+        for b in (1, 3, n):
+            c_bf, E_bf = bruteforce.alg2(n, A, xy0, 3, b, K=1.3, R=0.7,
+                                         repulse_neighbors=bool(flags), a=a, r=r)
+            c_or, E_or, _ = oracle.layout(n, rp, ci, xy0, iters=3, batch=b, K=1.3, C=0.7,
+                                          flags=flags, a=a, r=r)
+            np.testing.assert_allclose(c_or, np.array(c_bf), rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(E_or, E_bf, rtol=1e-9)
+
+
+@pytest.mark.parametrize("ar", [(1.0, -1.0), (3.0, -1.0), (2.0, -2.0), (1.5, -0.5)])
+@pytest.mark.parametrize("flags", [0, oracle.REPULSE_NEIGHBORS])
+def test_cycle_closed_form_general_model(ar, flags):
+    """Regular n-gon equilibrium of the (a, r) model.  With edge l and the
+    other vertices at d_k = l s_k, s_k = sin(pi k/n)/sin(pi/n): each vertex
+    feels an inward pull l^(a+1)/(K rho) from its two springs and an outward
+    push C K^2 d_k^(r+1)/(2 rho) from each repelling vertex, so
+    l^(a-r) = (C K^3 / 2) sum_k s_k^(r+1) (k = 2..n-2, or 1..n-1 when
+    neighbours repel).  For (2, -1) this is pin P1."""
+    a, r = ar
+    n, K, C = 6, 1.2, 0.8
+    ks = np.arange(1, n) if flags else np.arange(2, n - 1)
+    S = np.sum((np.sin(np.pi * ks / n) / np.sin(np.pi / n)) ** (r + 1))
+    ell = (C * K ** 3 / 2 * S) ** (1 / (a - r))
+    g = cycle_graph(n)
+    xy0 = _circle(n, 0.05, seed=n) * ell
+    xy, E, _ = oracle.layout(n, g.rowptr, g.colidx, xy0, iters=4000, batch=1, K=K, C=C,
+                             cooling=0.99, flags=flags, a=a, r=r)
+    edge = np.hypot(*(xy - np.roll(xy, -1, axis=0)).T)
+    np.testing.assert_allclose(edge, ell, rtol=1e-7)
