@@ -23,6 +23,7 @@ _SRC = os.path.join(_HERE, "bl_oracle.c")
 _IMPL = os.path.join(_HERE, "bl_oracle_impl.h")
 _BH = os.path.join(_HERE, "bl_oracle_bh.h")
 _INIT = os.path.join(_HERE, "bl_oracle_init.h")
+_METRICS = os.path.join(_HERE, "bl_oracle_metrics.h")
 _SO = os.path.join(_HERE, "libbl_oracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -33,7 +34,7 @@ REPULSE_NEIGHBORS = 1
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc: -O2 -ffp-contract=off, no fast-math."""
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_IMPL), os.path.getmtime(_BH),
-                 os.path.getmtime(_INIT))
+                 os.path.getmtime(_INIT), os.path.getmtime(_METRICS))
     if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= newest:
         return _SO
     tmp = _SO + f".tmp{os.getpid()}"
@@ -73,6 +74,12 @@ def _load():
         lib.oracle_bh_tree.restype = ctypes.c_int
         lib.oracle_set_model.argtypes = [dbl, dbl]
         lib.oracle_set_model.restype = None
+        lib.oracle_stress.argtypes = [i32, vp, vp, vp, vp, i32, vp, vp, vp, vp]
+        lib.oracle_stress.restype = ctypes.c_int
+        lib.oracle_edge_uniformity.argtypes = [i32, vp, vp, vp, vp]
+        lib.oracle_edge_uniformity.restype = ctypes.c_int
+        lib.oracle_neighborhood_preservation.argtypes = [i32, vp, vp, vp, vp, i32, vp, vp, vp]
+        lib.oracle_neighborhood_preservation.restype = ctypes.c_int
         lib.oracle_greedy_init.argtypes = [i32, vp, vp, i32, vp]
         lib.oracle_greedy_init.restype = ctypes.c_int
         del ll
@@ -238,3 +245,53 @@ def greedy_init(n, rowptr, colidx, root=0):
     if lib.oracle_greedy_init(n, _ptr(rowptr), _ptr(colidx), int(root), _ptr(out)) != 0:
         raise ValueError("oracle_greedy_init: invalid arguments")
     return out
+
+
+# ------------------------------------------------------------ quality metrics (§3.7)
+def stress(n, rowptr, colidx, xy, sources=None):
+    """M1: (scale-optimised stress, optimal scale s*, reachable ordered pairs,
+    unreachable pairs) over sources (all vertices if None)."""
+    lib = _load()
+    rowptr, colidx = _csr(rowptr, colidx)
+    c = np.ascontiguousarray(np.asarray(xy, np.float32).reshape(n, 2))
+    src = None if sources is None else np.ascontiguousarray(sources, np.int32)
+    st, sc = ctypes.c_double(0), ctypes.c_double(0)
+    pr, un = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    rc = lib.oracle_stress(n, _ptr(rowptr), _ptr(colidx), _ptr(c),
+                           None if src is None else _ptr(src), 0 if src is None else src.size,
+                           ctypes.byref(st), ctypes.byref(sc), ctypes.byref(pr), ctypes.byref(un))
+    if rc != 0:
+        raise ValueError("oracle_stress: invalid arguments")
+    return st.value, sc.value, pr.value, un.value
+
+
+def edge_uniformity(n, rowptr, colidx, xy):
+    """M2."""
+    lib = _load()
+    rowptr, colidx = _csr(rowptr, colidx)
+    c = np.ascontiguousarray(np.asarray(xy, np.float32).reshape(n, 2))
+    eu = ctypes.c_double(0)
+    if lib.oracle_edge_uniformity(n, _ptr(rowptr), _ptr(colidx), _ptr(c), ctypes.byref(eu)) != 0:
+        raise ValueError("oracle_edge_uniformity: invalid arguments")
+    return eu.value
+
+
+def neighborhood_preservation(n, rowptr, colidx, xy, queries=None, per_vertex=False):
+    """M3: (NP, vertices counted[, per-query Jaccard])."""
+    lib = _load()
+    rowptr, colidx = _csr(rowptr, colidx)
+    c = np.ascontiguousarray(np.asarray(xy, np.float32).reshape(n, 2))
+    q = None if queries is None else np.ascontiguousarray(queries, np.int32)
+    nq = n if q is None else q.size
+    jac = np.zeros(max(nq, 1), np.float64)
+    npv = ctypes.c_double(0)
+    cnt = ctypes.c_int32(0)
+    rc = lib.oracle_neighborhood_preservation(n, _ptr(rowptr), _ptr(colidx), _ptr(c),
+                                              None if q is None else _ptr(q),
+                                              0 if q is None else q.size, ctypes.byref(npv),
+                                              ctypes.byref(cnt), _ptr(jac))
+    if rc != 0:
+        raise ValueError("oracle_neighborhood_preservation: invalid arguments")
+    if per_vertex:
+        return npv.value, cnt.value, jac[:nq]
+    return npv.value, cnt.value

@@ -64,6 +64,9 @@ void oracle_set_model(double a, double r) {
 /* Greedy initialisation (Alg. 3) */
 #include "bl_oracle_init.h"
 
+/* Quality metrics (§3.7) */
+#include "bl_oracle_metrics.h"
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
