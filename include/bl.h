@@ -145,6 +145,33 @@ bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int32_t count, 
  * h's last stream.  *visits = 0 after an exact-algorithm call. */
 bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits);
 
+/* ---- layout quality metrics, §3.7; readings M1-M4 in DESIGN.md §3.
+ * All take the device layout d_xy (float2[n] of h's graph), run on cuda_stream
+ * and return synchronously; results are bitwise reproducible. */
+
+/* Edge uniformity: sqrt(sum_e (l_e - l_mu)^2 / (|E| l_mu^2)), each
+ * undirected edge once; 0 for a graph without edges. */
+bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu, void *cuda_stream);
+
+/* Scale-optimised stress: sum over ordered pairs (i, j), i in the
+ * source set, j != i reachable, of (s ||c_i - c_j|| - d_ij)^2 / d_ij^2 with
+ * d_ij = BFS hop distance and s = s* minimising it (closed form).  sources:
+ * host int32[nsrc] (NULL = all n vertices, nsrc ignored); scale (nullable) <-
+ * s*; pairs (nullable) <- reachable pairs; unreachable (nullable) <- pairs
+ * excluded because j is not reachable from i.  BL_EINVAL on a bad source. */
+bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sources, int32_t nsrc,
+                    double *stress, double *scale, long long *pairs, long long *unreachable,
+                    void *cuda_stream);
+
+/* Neighbourhood preservation (reading M3): mean over the query
+ * vertices i with deg(i) = k > 0 of the Jaccard similarity between N(i) and
+ * the k layout-nearest other vertices (fp32 squared distances, ties by vertex
+ * id).  queries: host int32[nq] (NULL = all vertices); counted (nullable) <-
+ * the number of queries with k > 0. */
+bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy, const int32_t *queries,
+                                       int32_t nq, double *np, int32_t *counted,
+                                       void *cuda_stream);
+
 /* Largest n the resident design accepts on the current device. */
 int32_t bl_max_vertices(void);
 

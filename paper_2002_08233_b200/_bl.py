@@ -66,6 +66,13 @@ def _load() -> ctypes.CDLL:
     lib.bl_last_launch_count.restype = i32
     lib.bl_greedy_init.argtypes = [i32, vp, vp, i32, vp]
     lib.bl_greedy_init.restype = ctypes.c_int
+    lib.bl_edge_uniformity.argtypes = [vp, vp, P(ctypes.c_double), vp]
+    lib.bl_edge_uniformity.restype = ctypes.c_int
+    lib.bl_stress.argtypes = [vp, vp, vp, i32, P(ctypes.c_double), P(ctypes.c_double),
+                              P(ctypes.c_longlong), P(ctypes.c_longlong), vp]
+    lib.bl_stress.restype = ctypes.c_int
+    lib.bl_neighborhood_preservation.argtypes = [vp, vp, vp, i32, P(ctypes.c_double), P(i32), vp]
+    lib.bl_neighborhood_preservation.restype = ctypes.c_int
     lib.bl_last_visits.argtypes = [vp, P(ctypes.c_ulonglong)]
     lib.bl_last_visits.restype = ctypes.c_int
     lib.bl_kernel_name.argtypes = [vp]
@@ -87,7 +94,8 @@ lib = _load()
 
 # symbols include/bl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bl_params_default", "bl_greedy_init", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
-           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_microbench",
+           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_edge_uniformity",
+           "bl_stress", "bl_neighborhood_preservation", "bl_microbench",
            "bl_debug_profile", "bl_destroy", "bl_status_string", "bl_last_error")
 
 
@@ -183,6 +191,37 @@ def bl_greedy_init(n: int, rowptr, colidx, root: int = 0) -> np.ndarray:
     if rc != BL_OK:
         raise BLError(rc, f"{lib.bl_status_string(rc).decode()}: bl_greedy_init")
     return out
+
+
+def bl_edge_uniformity(h: int, d_xy, stream=0) -> float:
+    s = getattr(stream, "cuda_stream", stream)
+    eu = ctypes.c_double(0)
+    _check(lib.bl_edge_uniformity(h, _ptr(d_xy), ctypes.byref(eu), s or None), h)
+    return eu.value
+
+
+def bl_stress(h: int, d_xy, sources=None, stream=0):
+    """(stress, s*, reachable pairs, unreachable pairs)."""
+    s = getattr(stream, "cuda_stream", stream)
+    src = None if sources is None else np.ascontiguousarray(sources, dtype=np.int32)
+    st, sc = ctypes.c_double(0), ctypes.c_double(0)
+    pr, un = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    _check(lib.bl_stress(h, _ptr(d_xy), None if src is None else src.ctypes.data,
+                         0 if src is None else src.size, ctypes.byref(st), ctypes.byref(sc),
+                         ctypes.byref(pr), ctypes.byref(un), s or None), h)
+    return st.value, sc.value, pr.value, un.value
+
+
+def bl_neighborhood_preservation(h: int, d_xy, queries=None, stream=0):
+    """(NP, vertices counted)."""
+    s = getattr(stream, "cuda_stream", stream)
+    q = None if queries is None else np.ascontiguousarray(queries, dtype=np.int32)
+    npv = ctypes.c_double(0)
+    cnt = ctypes.c_int32(0)
+    _check(lib.bl_neighborhood_preservation(h, _ptr(d_xy), None if q is None else q.ctypes.data,
+                                            0 if q is None else q.size, ctypes.byref(npv),
+                                            ctypes.byref(cnt), s or None), h)
+    return npv.value, cnt.value
 
 
 def bl_last_visits(h: int) -> int:
