@@ -379,8 +379,11 @@ def phase_profile(g, xy0, params, dev, mhz):
     torch.cuda.synchronize()
     pr = bl.bl_debug_profile(lay.h).astype(np.float64) / mhz  # cycles -> us
     lay.close()
-    names = ["attraction", "repulsion_sweep", "cta_combine", "barrier1_wait", "update",
-             "barrier2_wait", "tail", "unused"]
+    # pipelined driver: slot 0 = barrier ph-1 + detection until control is
+    # claimed, 1 = warp 0's task loop, 2 = in-CTA tail + combine, 3 = loop
+    # glue, 4 = control task, 5 = arrive, 7 = update tasks after control
+    names = ["barrier_to_control", "tasks_warp0", "cta_tail_combine", "glue", "control",
+             "arrive", "end", "updates_after_control"]
     busy = pr[8:]
     return {"cta0_us": {k: round(float(v), 1) for k, v in zip(names, pr[:8])},
             "phaseR_busy_us": {"min": float(busy.min()), "median": float(np.median(busy)),

@@ -579,12 +579,17 @@ struct BLShared {
   double e_acc;   // this CTA's energy of the running iteration
   double e_task[BL_ETASK_MAX];
   double e_warp[BL_NW_MAX];
+  // profile timestamps (BL_PROFILE=1): phase start, control claimed /
+  // published, last update task done
+  long long ts_start, ts_claim, ts_ready, ts_upd;
 };
 
-__device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, BLShared &sh) {
+__device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, BLShared &sh,
+                                               bool prof = false) {
   __syncthreads();
   target += gridDim.x;  // every thread tracks the barrier target
   if (threadIdx.x == 0) {
+    if (prof) sh.ts_start = clock64();
     sh.unit_ctr = 0;
     sh.u_next = 0;
     sh.u_done = 0;
@@ -704,6 +709,7 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
   int go = 0;
   if (lane == 0 && (int)(bl_ld_acquire(p.bar) - bar_target) >= 0)
     go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
+  if (go && p.prof) sh.ts_claim = clock64();
   go = __shfl_sync(0xffffffffu, go, 0);
   if (!go) return;
   __syncwarp();  // order the lanes' reads after lane 0's acquire
@@ -730,6 +736,7 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
   if (lane == 0) {
     if (stop) *(volatile int *)&sh.stop_flag = 1;
     __threadfence_block();
+    if (p.prof) sh.ts_ready = clock64();
     *(volatile int *)&sh.ready = f.ph;
   }
   __syncwarp();
@@ -750,7 +757,7 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
-    atomicAdd(&sh.u_done, 1);
+    if (atomicAdd(&sh.u_done, 1) == f.owned - 1 && p.prof) sh.ts_upd = clock64();
   }
   return true;
 }
@@ -846,6 +853,13 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
     bl_phase_tasks<T, TP>(p, f, src4, tgt + (ph & 1) * BL_TGT_CAP, red, sh, bar_target);
     pf.mark(1);
     __syncthreads();
+    if (pf.on && ph > 0) {
+      // critical-path split of this phase (CTA 0 reported): barrier ph-1 +
+      // its detection, control task, update tasks after control
+      pf.acc[0] += (unsigned long long)(sh.ts_claim - sh.ts_start);
+      pf.acc[4] += (unsigned long long)(sh.ts_ready - sh.ts_claim);
+      if (f.owned > 0) pf.acc[7] += (unsigned long long)(sh.ts_upd - sh.ts_ready);
+    }
     if (sh.stop_flag) {
       if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
       pf.flush(p);
@@ -868,7 +882,7 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
     }
     pf.mark(2);
     asm volatile("cp.async.wait_all;" ::: "memory");
-    if (ph <= P) bl_grid_arrive(p.bar, bar_target, sh);
+    if (ph <= P) bl_grid_arrive(p.bar, bar_target, sh, p.prof != nullptr);
     pf.mark(5);
   }
   if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
