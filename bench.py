@@ -379,9 +379,9 @@ def phase_profile(g, xy0, params, dev, mhz):
     torch.cuda.synchronize()
     pr = bl.bl_debug_profile(lay.h).astype(np.float64) / mhz  # cycles -> us
     lay.close()
-    # pipelined driver: slot 0 = barrier ph-1 + detection until control is
-    # claimed, 1 = warp 0's task loop, 2 = in-CTA tail + combine, 3 = loop
-    # glue, 4 = control task, 5 = arrive, 7 = update tasks after control
+    # pipelined driver: 1 = warp 0's task loop, 2 = in-CTA tail + combine,
+    # 3 = loop glue, 5 = arrive; 0, 4, 7 (barrier-to-control, control, updates
+    # after control) only in a -DBL_PHASE_TS build
     names = ["barrier_to_control", "tasks_warp0", "cta_tail_combine", "glue", "control",
              "arrive", "end", "updates_after_control"]
     busy = pr[8:]

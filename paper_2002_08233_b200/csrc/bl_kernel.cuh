@@ -32,6 +32,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 // threads per CTA: a template parameter of the kernel (NT, launch bounds);
 // device code reads it as blockDim.x.  BL_NT / BL_NW: the runtime values.
 #define BL_NT ((int)blockDim.x)
@@ -236,7 +238,9 @@ __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0
 // f_a(d)/d = d^(a-1)/K plus, in the if/else model, the removal of the
 // all-pairs repulsion rep * d^(r-1) (rep = C K^2, or 0 with
 // BL_REPULSE_NEIGHBORS).  rs = 1/d.
+template <bool FAST>
 __device__ __forceinline__ float bl_model_coef(const BLKParams &p, float d2, float rs, float rep) {
+  if (FAST) return fmaf(rep * rs, rs, d2 * rs * p.invK);  // (a, r) = (2, -1)
   float at;
   switch (p.amode) {
     case 0: at = d2 * rs; break;  // a = 2 (the paper's FR model)
@@ -462,17 +466,21 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
       const float2 ci = __ldcg(p.xy + v);
       float sx = 0.f, sy = 0.f;
       const float rep = (p.flags & 1u) ? 0.f : p.ck2;
+      auto scan_row = [&](auto fast) {
 #pragma unroll 4
-      for (int k = k0 + lane; k < k1; k += 32) {
-        const int j = __ldg(p.colidx + k);
-        const float2 cj = __ldcg(p.xy + j);
-        const float dx = cj.x - ci.x, dy = cj.y - ci.y;
-        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
-        const float rs = bl_rsqrt(d2);
-        const float coef = bl_model_coef(p, d2, rs, rep);
-        sx = fmaf(coef, dx, sx);
-        sy = fmaf(coef, dy, sy);
-      }
+        for (int k = k0 + lane; k < k1; k += 32) {
+          const int j = __ldg(p.colidx + k);
+          const float2 cj = __ldcg(p.xy + j);
+          const float dx = cj.x - ci.x, dy = cj.y - ci.y;
+          const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+          const float rs = bl_rsqrt(d2);
+          const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+          sx = fmaf(coef, dx, sx);
+          sy = fmaf(coef, dy, sy);
+        }
+      };
+      if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});  // branch hoisted out of the loop
+      else scan_row(std::false_type{});
       sx = bl_warp_sum0(sx);
       sy = bl_warp_sum0(sy);
       if (lane == 0) p.attr[it - ib] = make_float2(sx, sy);
@@ -579,9 +587,12 @@ struct BLShared {
   double e_acc;   // this CTA's energy of the running iteration
   double e_task[BL_ETASK_MAX];
   double e_warp[BL_NW_MAX];
-  // profile timestamps (BL_PROFILE=1): phase start, control claimed /
-  // published, last update task done
+#ifdef BL_PHASE_TS
+  // critical-path timestamps (profiling builds, -DBL_PHASE_TS; they cost ~3 %
+  // at C5 even when disabled at run time, so they are compiled out by
+  // default): phase start, control claimed / published, last update done
   long long ts_start, ts_claim, ts_ready, ts_upd;
+#endif
 };
 
 __device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, BLShared &sh,
@@ -589,7 +600,9 @@ __device__ __forceinline__ void bl_grid_arrive(unsigned *bar, unsigned &target, 
   __syncthreads();
   target += gridDim.x;  // every thread tracks the barrier target
   if (threadIdx.x == 0) {
+#ifdef BL_PHASE_TS
     if (prof) sh.ts_start = clock64();
+#endif
     sh.unit_ctr = 0;
     sh.u_next = 0;
     sh.u_done = 0;
@@ -657,17 +670,21 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
   const int k0 = __ldg(p.rowptr + v), k1 = __ldg(p.rowptr + v + 1);
   const float rep = (p.flags & 1u) ? 0.f : p.ck2;
   float sx = 0.f, sy = 0.f;
+  auto scan_row = [&](auto fast) {
 #pragma unroll 4
-  for (int k = k0 + lane; k < k1; k += 32) {
-    const int j = __ldg(p.colidx + k);
-    const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
-    const float dx = cj.x - ci.x, dy = cj.y - ci.y;
-    const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
-    const float rs = bl_rsqrt(d2);
-    const float coef = bl_model_coef(p, d2, rs, rep);
-    sx = fmaf(coef, dx, sx);
-    sy = fmaf(coef, dy, sy);
-  }
+    for (int k = k0 + lane; k < k1; k += 32) {
+      const int j = __ldg(p.colidx + k);
+      const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+      const float dx = cj.x - ci.x, dy = cj.y - ci.y;
+      const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+      const float rs = bl_rsqrt(d2);
+      const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+      sx = fmaf(coef, dx, sx);
+      sy = fmaf(coef, dy, sy);
+    }
+  };
+  if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});  // branch hoisted out of the loop
+  else scan_row(std::false_type{});
   rx = bl_warp_sum0(rx);
   ry = bl_warp_sum0(ry);
   sx = bl_warp_sum0(sx);
@@ -709,7 +726,9 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
   int go = 0;
   if (lane == 0 && (int)(bl_ld_acquire(p.bar) - bar_target) >= 0)
     go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
+#ifdef BL_PHASE_TS
   if (go && p.prof) sh.ts_claim = clock64();
+#endif
   go = __shfl_sync(0xffffffffu, go, 0);
   if (!go) return;
   __syncwarp();  // order the lanes' reads after lane 0's acquire
@@ -736,7 +755,9 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
   if (lane == 0) {
     if (stop) *(volatile int *)&sh.stop_flag = 1;
     __threadfence_block();
+#ifdef BL_PHASE_TS
     if (p.prof) sh.ts_ready = clock64();
+#endif
     *(volatile int *)&sh.ready = f.ph;
   }
   __syncwarp();
@@ -757,7 +778,11 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
+#ifdef BL_PHASE_TS
     if (atomicAdd(&sh.u_done, 1) == f.owned - 1 && p.prof) sh.ts_upd = clock64();
+#else
+    atomicAdd(&sh.u_done, 1);
+#endif
   }
   return true;
 }
@@ -853,6 +878,7 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
     bl_phase_tasks<T, TP>(p, f, src4, tgt + (ph & 1) * BL_TGT_CAP, red, sh, bar_target);
     pf.mark(1);
     __syncthreads();
+#ifdef BL_PHASE_TS
     if (pf.on && ph > 0) {
       // critical-path split of this phase (CTA 0 reported): barrier ph-1 +
       // its detection, control task, update tasks after control
@@ -860,6 +886,7 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
       pf.acc[4] += (unsigned long long)(sh.ts_ready - sh.ts_claim);
       if (f.owned > 0) pf.acc[7] += (unsigned long long)(sh.ts_upd - sh.ts_ready);
     }
+#endif
     if (sh.stop_flag) {
       if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
       pf.flush(p);
