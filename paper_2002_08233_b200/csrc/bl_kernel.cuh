@@ -582,6 +582,9 @@ struct BLShared {
   int stop_flag;  // tol convergence reached
   int ready;      // last phase whose control work is done
   int ctrl_claim; // last phase whose control work was claimed
+  int seen;       // last phase whose barrier ph-1 was observed complete: the
+                  // update tasks only need that (they read pend, not the
+                  // commits of the control task), so they run alongside it
   int done_iters;
   double e_prev;  // energy of the previous completed iteration
   double e_acc;   // this CTA's energy of the running iteration
@@ -729,6 +732,10 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
 #ifdef BL_PHASE_TS
   if (go && p.prof) sh.ts_claim = clock64();
 #endif
+  if (go) {
+    *(volatile int *)&sh.seen = f.ph;  // release the update tasks now
+    __threadfence_block();
+  }
   go = __shfl_sync(0xffffffffu, go, 0);
   if (!go) return;
   __syncwarp();  // order the lanes' reads after lane 0's acquire
@@ -768,7 +775,7 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
                                               BLShared &sh) {
   const int lane = threadIdx.x & 31;
   const volatile BLShared &vs = sh;
-  if (vs.ready != f.ph || vs.stop_flag || vs.u_next >= f.owned) return false;
+  if (vs.seen != f.ph || vs.stop_flag || vs.u_next >= f.owned) return false;
   int t = f.owned;
   if (lane == 0) t = atomicAdd(&sh.u_next, 1);
   t = __shfl_sync(0xffffffffu, t, 0);
@@ -817,7 +824,7 @@ __device__ __forceinline__ void bl_phase_tasks(const BLKParams &p, const BLPhase
         for (;;) {
           if (f.ph > 0 && vs.ready != f.ph) bl_try_control(p, f, src4, sh, bar_target);
           if (bl_try_update(p, f, src4, sh)) continue;
-          if ((f.ph == 0 || vs.ready == f.ph) && (vs.stop_flag || vs.u_done >= f.owned)) break;
+          if ((f.ph == 0 || vs.seen == f.ph) && (vs.stop_flag || vs.u_done >= f.owned)) break;
           __nanosleep(64);
         }
         __threadfence_block();
@@ -931,6 +938,7 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
     sh.stop_flag = 0;
     sh.ready = 0;
     sh.ctrl_claim = 0;
+    sh.seen = 0;
   }
   int *unit_ctr = &sh.unit_ctr;
   double *e_warp = sh.e_warp;
