@@ -159,11 +159,16 @@ extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t 
   return m;
 }
 
+// static shared memory of the layout kernel (BLShared + locals), reserved
+// out of the opt-in maximum before the dynamic buffers are sized
+static const int kStaticSmemReserve = (int)sizeof(BLShared) + 1024;
+
 static int red_cap_for(int chunk4) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const long long room = (long long)optin - 1024 - (long long)bl_smem_bytes(chunk4, 0);
+  const long long room =
+      (long long)optin - 1024 - kStaticSmemReserve - (long long)bl_smem_bytes(chunk4, 0);
   long long cap = room / 8;
   if (cap > BL_RED_MAX) cap = BL_RED_MAX;
   return (int)cap;
@@ -206,7 +211,8 @@ extern "C" int32_t bl_max_vertices(void) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return 0;
-  const long long room = (long long)optin - 2048 - (long long)bl_smem_bytes(0, BL_RED_MIN);
+  const long long room =
+      (long long)optin - 2048 - kStaticSmemReserve - (long long)bl_smem_bytes(0, BL_RED_MIN);
   const long long per = room / (long long)sizeof(float4) * 2;
   const long long n = per * sms;
   return (int32_t)std::min<long long>(n, 0x7fffffff);

@@ -590,6 +590,13 @@ struct BLShared {
   double e_acc;   // this CTA's energy of the running iteration
   double e_task[BL_ETASK_MAX];
   double e_warp[BL_NW_MAX];
+  // CSR rows (<= 32 entries) of this CTA's owned vertices of a batch, staged
+  // by the control task of the phase that sweeps the batch, used by the
+  // update tasks one phase later (two fewer dependent L2 round trips on the
+  // per-batch critical path); rowq = the batch they belong to
+  int rows[2][BL_ETASK_MAX][32];
+  int rdeg[2][BL_ETASK_MAX];
+  int rowq[2];
 #ifdef BL_PHASE_TS
   // critical-path timestamps (profiling builds, -DBL_PHASE_TS; they cost ~3 %
   // at C5 even when disabled at run time, so they are compiled out by
@@ -650,7 +657,8 @@ __device__ __forceinline__ double bl_energy_sum_warp(const BLKParams &p, int it)
 
 // Update of one owned vertex v of batch q (warp-cooperative); ||f||^2 -> *eq.
 __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, double stepd,
-                                              float4 *src4, double *eq) {
+                                              float4 *src4, double *eq, const int *srow,
+                                              int sdeg) {
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b;
   const int local = v - lo;
@@ -670,10 +678,27 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     rx += t.x;
     ry += t.y;
   }
-  const int k0 = __ldg(p.rowptr + v), k1 = __ldg(p.rowptr + v + 1);
+  int k0 = 0, k1 = 0;
+  if (!srow) {
+    k0 = __ldg(p.rowptr + v);
+    k1 = __ldg(p.rowptr + v + 1);
+  }
   const float rep = (p.flags & 1u) ? 0.f : p.ck2;
   float sx = 0.f, sy = 0.f;
   auto scan_row = [&](auto fast) {
+    if (srow) {  // staged row: one entry per lane
+      if (lane < sdeg) {
+        const int j = srow[lane];
+        const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        const float dx = cj.x - ci.x, dy = cj.y - ci.y;
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+        const float rs = bl_rsqrt(d2);
+        const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+        sx = fmaf(coef, dx, sx);
+        sy = fmaf(coef, dy, sy);
+      }
+      return;
+    }
 #pragma unroll 4
     for (int k = k0 + lane; k < k1; k += 32) {
       const int j = __ldg(p.colidx + k);
@@ -720,6 +745,25 @@ __device__ __forceinline__ bool bl_closes_iteration(int q, int nb, int P) {
   return q % nb == nb - 1 || q == P - 1;
 }
 
+// Stage the CSR rows of this CTA's owned vertices of batch q (swept in this
+// phase, updated in the next) into shared memory: rows of <= 32 entries,
+// rdeg = -1 marks longer rows (they take the global path).
+__device__ __forceinline__ void bl_stage_rows_warp(const BLKParams &p, int q, BLShared &sh) {
+  const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
+  const int lo = (q % p.nb) * p.b, hi = min(lo + p.b, p.n);
+  const int v0 = lo + ((c - lo % G) + G) % G;
+  const int owned = v0 < hi ? (hi - 1 - v0) / G + 1 : 0;
+  const int buf = q & 1;
+  for (int t = 0; t < owned; ++t) {
+    const int v = v0 + t * G;
+    const int k0 = __ldg(p.rowptr + v), deg = __ldg(p.rowptr + v + 1) - k0;
+    if (deg <= 32 && lane < deg) sh.rows[buf][t][lane] = __ldg(p.colidx + k0 + lane);
+    if (lane == 0) sh.rdeg[buf][t] = deg <= 32 ? deg : -1;
+  }
+  __syncwarp();
+  if (lane == 0) sh.rowq[buf] = q;
+}
+
 // Control work of phase ph, attempted by a warp between tasks: if barrier
 // ph-1 has completed and no other warp claimed it, do (a)-(c) and publish.
 __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase &f,
@@ -758,6 +802,7 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
     const int lo_n = ((f.ph + 1) % nb) * p.b;
     bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), f.tgt_next);
   }
+  if (!stop && f.ph < f.P) bl_stage_rows_warp(p, f.ph, sh);
   __syncwarp();
   if (lane == 0) {
     if (stop) *(volatile int *)&sh.stop_flag = 1;
@@ -781,7 +826,11 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
   t = __shfl_sync(0xffffffffu, t, 0);
   if (t >= f.owned) return false;
   __threadfence_block();  // acquire the control warp's publication
-  bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t]);
+  const int buf = f.q1 & 1;
+  const volatile BLShared &vsh = sh;
+  const bool staged = vsh.rowq[buf] == f.q1 && vsh.rdeg[buf][t] >= 0;
+  bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t],
+                staged ? sh.rows[buf][t] : nullptr, staged ? vsh.rdeg[buf][t] : 0);
   __syncwarp();
   if (lane == 0) {
     __threadfence_block();
@@ -939,6 +988,7 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
     sh.ready = 0;
     sh.ctrl_claim = 0;
     sh.seen = 0;
+    sh.rowq[0] = sh.rowq[1] = -1;
   }
   int *unit_ctr = &sh.unit_ctr;
   double *e_warp = sh.e_warp;
