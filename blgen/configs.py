@@ -38,6 +38,9 @@ CONFIGS: dict[str, LayoutConfig] = {
     "C3b1024": LayoutConfig("C3b1024", "triangulated mesh 100x110 (11,000 vertices), batch 1024", 1024, 600),
     "C4": LayoutConfig("C4", "R-MAT scale 15, edge factor 16 (32,768 vertices)", 256, 600),
     "C5": LayoutConfig("C5", "R-MAT scale 18, edge factor 8 (262,144 vertices)", 1024, 50),
+    # beyond BASELINE.json: a 2^20-vertex graph, the size class where the paper
+    # runs only BatchLayoutBH; used for the BH measurements
+    "C6": LayoutConfig("C6", "R-MAT scale 20, edge factor 8 (1,048,576 vertices)", 1024, 20),
 }
 
 RMAT_ABCD = (0.57, 0.19, 0.19)
@@ -61,6 +64,8 @@ def _graph(name: str) -> graphs.CSRGraph:
         return graphs.rmat_graph(15, 16, *RMAT_ABCD, seed=cfg.graph_seed)
     if base == "C5":
         return graphs.rmat_graph(18, 8, *RMAT_ABCD, seed=cfg.graph_seed)
+    if base == "C6":
+        return graphs.rmat_graph(20, 8, *RMAT_ABCD, seed=cfg.graph_seed)
     raise KeyError(name)
 
 

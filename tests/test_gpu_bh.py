@@ -175,3 +175,23 @@ def test_exact_path_unchanged_by_algo_field():
             lay.layout_device(d, iters=1, batch=256, algo=7)
         with pytest.raises(bl.BLError):
             lay.layout_device(d, iters=1, batch=256, algo=BH, theta=-1.0)
+
+
+def test_C6_million_vertices_shadowed():
+    """2^20 vertices (C6), the size class where the paper runs only
+    BatchLayoutBH: batches 0, 1 and 700 of the first iteration from the GPU's
+    own state against the oracle, and the exact visit count of batch 0."""
+    g, xy0, cfg = build_config("C6")
+    b = cfg.batch
+    for t in (0, 1, 700):
+        s_t = xy0 if t == 0 else gpu_layout(g, xy0, iters=1, batch=b, max_batches=t, **_bh())[0]
+        s_t1 = gpu_layout(g, xy0, iters=1, batch=b, max_batches=t + 1, **_bh())[0]
+        lo, hi = t * b, (t + 1) * b
+        assert np.array_equal(s_t1[:lo], s_t[:lo]) and np.array_equal(s_t1[hi:], s_t[hi:])
+        f, _ = oracle.bh_forces(g.n, g.rowptr, g.colidx, xy0, s_t, lo, hi - lo)
+        ref = s_t.astype(np.float64).copy()
+        ref[lo:hi] += f / np.hypot(f[:, 0], f[:, 1])[:, None]
+        assert_positions_close(s_t1, ref, what=f"BH C6 batch {t}")
+    got, visits = gpu_forces(g, xy0, 0, b, with_visits=True, **_bh())
+    _, ref_visits = oracle.bh_forces(g.n, g.rowptr, g.colidx, xy0, xy0, 0, b)
+    assert visits == ref_visits

@@ -392,3 +392,16 @@ def test_one_batch_repeated(name):
         if first is None:
             first = got
         assert np.array_equal(got, first)
+
+
+def test_C6_million_vertices_one_batch():
+    """The exact kernel at 2^20 vertices (resident sources 57 KB per CTA):
+    one batch of 1,024 targets against all 1,048,575 sources vs the oracle."""
+    g, xy0, cfg = build_config("C6")
+    got, _, _ = gpu_layout(g, xy0, **_params(cfg, iters=1, max_batches=1))
+    b = cfg.batch
+    f = oracle.forces(g.n, g.rowptr, g.colidx, xy0, 0, b)
+    ref = xy0.astype(np.float64).copy()
+    ref[:b] += f / np.hypot(f[:, 0], f[:, 1])[:, None]
+    assert_positions_close(got, ref, what="C6 one batch")
+    assert np.array_equal(got[b:], xy0[b:])
