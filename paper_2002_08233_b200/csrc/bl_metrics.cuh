@@ -38,15 +38,35 @@ __device__ __forceinline__ double blm_block_sum(double v, double *sh_warp) {
 // ---------------------------------------------------------------- EU (M2)
 // pass 0: part[b] = (sum of edge lengths, edge count); pass 1: part[b] =
 // sum (l - mu)^2 with mu = stats[0] / stats[1] from pass 0.
+// Edge-parallel: thread t owns the contiguous CSR entries [t*chunk, ...)
+// (balanced whatever the degree skew), finds its first row by binary search
+// over rowptr and walks on; fixed mapping -> deterministic sums.
 __global__ void __launch_bounds__(BLM_NT) blm_eu_pass(const int *rowptr, const int *colidx,
                                                       const float2 *xy, int n, int pass,
                                                       const double *stats, double2 *part) {
   __shared__ double sh[BLM_NW];
   double acc = 0.0, cnt = 0.0;
   const double mu = pass ? stats[0] / stats[1] : 0.0;
-  for (int i = blockIdx.x * BLM_NT + threadIdx.x; i < n; i += gridDim.x * BLM_NT) {
-    const float2 ci = xy[i];
-    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+  const long long nnz = rowptr[n];
+  const long long T = (long long)gridDim.x * BLM_NT;
+  const long long t = (long long)blockIdx.x * BLM_NT + threadIdx.x;
+  const long long chunk = (nnz + T - 1) / T;
+  const long long k0 = t * chunk, k1 = min(nnz, k0 + chunk);
+  if (k0 < k1) {
+    int lo = 0, hi = n - 1;  // largest i with rowptr[i] <= k0
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rowptr[mid] <= k0) lo = mid;
+      else hi = mid - 1;
+    }
+    int i = lo, end_i = rowptr[i + 1];
+    float2 ci = xy[i];
+    for (long long k = k0; k < k1; ++k) {
+      while (k >= end_i) {
+        ++i;
+        end_i = rowptr[i + 1];
+        ci = xy[i];
+      }
       const int j = colidx[k];
       if (j <= i) continue;
       const float2 cj = xy[j];
