@@ -35,6 +35,8 @@
 #define BH_NT 512
 #define BH_NW (BH_NT / 32)
 #define BH_FCAP 512  // frontier entries per buffer per warp
+#define BH_TOP_LEVEL 4  // tree levels 0..4 are copied to shared memory per CTA
+#define BH_TOP_MAX 352  // >= 1 + 4 + 16 + 64 + 256
 
 struct BHKParams {
   int n, b, nb, iters, max_batches;
@@ -85,6 +87,15 @@ struct BHShared {
   float D;
   float xmin, ymin, scale;
   int degenerate;
+  // the top of the tree (levels <= BH_TOP_LEVEL) in BFS order, per CTA: every
+  // query starts there, so its records come from shared memory instead of
+  // one L2 round trip per level after each grid barrier (which invalidates
+  // L1).  Node references: r >= 0 global pre-order index, r < 0 top slot -r-1
+  float4 topA[BH_TOP_MAX];
+  int4 topB[BH_TOP_MAX];
+  int4 topK[BH_TOP_MAX];  // child refs (internal) or (vertex id, -, -, -) (leaf)
+  int topG[BH_TOP_MAX];   // global index
+  int ntop;
 };
 
 __device__ __forceinline__ unsigned bh_interleave(unsigned qx, unsigned qy) {
@@ -456,6 +467,54 @@ __device__ void bh_build_tree(const BHKParams &p, BHShared &sh, unsigned &bar_ta
     }
     bl_grid_sync(p.bar, bar_target, unit_dummy);
   }
+  // B6: the top of the tree into shared memory (warp 0 of each CTA, BFS)
+  if (warp == 0) {
+    int n_top = 1, head = 0;
+    if (lane == 0) sh.topG[0] = 0;
+    __syncwarp();
+    while (head < n_top) {
+      const int i = head + lane;
+      int m = 0;
+      int4 B = make_int4(0, 0, 0, 0), C = make_int4(-1, -1, -1, -1);
+      int g = 0;
+      if (i < n_top) {
+        g = sh.topG[i];
+        B = __ldcg(p.nodeB + g);
+        C = __ldcg(p.nodeC + g);
+        sh.topA[i] = __ldcg(p.nodeA + g);
+        sh.topB[i] = B;
+        const bool leaf = B.x & (1 << 16);
+        if (!leaf && (B.x & 0xff) < BH_TOP_LEVEL) m = (B.x >> 8) & 0xff;
+      }
+      int incl = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int pos = n_top + incl - m;
+      if (i < n_top) {
+        const int kids[4] = {g + 1, C.x, C.y, C.z};
+        int4 K;
+        if (B.x & (1 << 16)) {
+          K = make_int4(C.w, -1, -1, -1);
+        } else if (m > 0) {  // children are top slots pos .. pos+m-1
+          for (int q = 0; q < m; ++q) sh.topG[pos + q] = kids[q];
+          K = make_int4(-(pos + 1), m > 1 ? -(pos + 2) : -1, m > 2 ? -(pos + 3) : -1,
+                        m > 3 ? -(pos + 4) : -1);
+        } else {  // children stay global
+          K = make_int4(kids[0], kids[1], kids[2], kids[3]);
+        }
+        sh.topK[i] = K;
+      }
+      const int added = __shfl_sync(0xffffffffu, incl, 31);
+      head = min(n_top, head + 32);
+      n_top += added;
+      __syncwarp();
+    }
+    if (lane == 0) sh.ntop = n_top;
+  }
+  __syncthreads();
   pf.mark(3);
 }
 
@@ -474,6 +533,36 @@ __device__ __forceinline__ BHNode bh_load(const BHKParams &p, int k) {
   nd.B = p.nodeB[k];
   nd.C = p.nodeC[k];
   return nd;
+}
+// A node by reference (shared top slot or global index): its record, its
+// child references, its global index.
+struct BHRefNode {
+  BHNode nd;
+  int kids[4];
+  int g;
+};
+__device__ __forceinline__ BHRefNode bh_load_ref(const BHKParams &p, const BHShared &sh, int r) {
+  BHRefNode x;
+  if (r < 0) {
+    const int i = -r - 1;
+    x.nd.A = sh.topA[i];
+    x.nd.B = sh.topB[i];
+    const int4 K = sh.topK[i];
+    x.nd.C = make_int4(-1, -1, -1, K.x);  // vertex id of a leaf in .w
+    x.kids[0] = K.x;
+    x.kids[1] = K.y;
+    x.kids[2] = K.z;
+    x.kids[3] = K.w;
+    x.g = sh.topG[i];
+  } else {
+    x.nd = bh_load(p, r);
+    x.kids[0] = r + 1;
+    x.kids[1] = x.nd.C.x;
+    x.kids[2] = x.nd.C.y;
+    x.kids[3] = x.nd.C.z;
+    x.g = r;
+  }
+  return x;
 }
 
 // Live coordinate of vertex j (reading B5): batch `pl` vertices [plo, phi)
@@ -623,22 +712,23 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
   // repulsion: frontier traversal from the root (Alg. S2)
   int *cur = sh.frontier[warp][0], *nxt = sh.frontier[warp][1];
   int ncur = 1;
-  if (lane == 0) cur[0] = 0;
+  if (lane == 0) cur[0] = -1;  // the root, top slot 0
   __syncwarp();
   while (ncur > 0) {
     int nnext = 0;
     for (int base = 0; base < ncur; base += 32) {
       const int idx = base + lane;
-      const int k = idx < ncur ? cur[idx] : -1;
+      const bool has = idx < ncur;
+      const int r = has ? cur[idx] : 0;
       int m = 0;
-      BHNode nd;
-      if (k >= 0) {
-        nd = bh_load(p, k);
+      BHRefNode x;
+      if (has) {
+        x = bh_load_ref(p, sh, r);
         ++vis;
-        if (nd.B.x & (1 << 16)) {
-          bh_leaf_terms(p, nd, v, cv.x, cv.y, plo, phi, pend, fx, fy);
-        } else if (!bh_mac(p, nd.A, cv.x, cv.y, fx, fy)) {
-          m = (nd.B.x >> 8) & 0xff;
+        if (x.nd.B.x & (1 << 16)) {
+          bh_leaf_terms(p, x.nd, v, cv.x, cv.y, plo, phi, pend, fx, fy);
+        } else if (!bh_mac(p, x.nd.A, cv.x, cv.y, fx, fy)) {
+          m = (x.nd.B.x >> 8) & 0xff;
         }
       }
       int incl = m;
@@ -651,12 +741,12 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
       const bool fits = pos + m <= BH_FCAP;
       if (m > 0) {
         if (fits) {
-          nxt[pos] = k + 1;
-          if (m > 1) nxt[pos + 1] = nd.C.x;
-          if (m > 2) nxt[pos + 2] = nd.C.y;
-          if (m > 3) nxt[pos + 3] = nd.C.z;
+          nxt[pos] = x.kids[0];
+          if (m > 1) nxt[pos + 1] = x.kids[1];
+          if (m > 2) nxt[pos + 2] = x.kids[2];
+          if (m > 3) nxt[pos + 3] = x.kids[3];
         } else {
-          bh_walk_subtree(p, k, nd.B.w, v, cv.x, cv.y, plo, phi, pend, fx, fy, vis);  // full
+          bh_walk_subtree(p, x.g, x.nd.B.w, v, cv.x, cv.y, plo, phi, pend, fx, fy, vis);  // full
         }
       }
       // entries written: the fitting lanes form a prefix of the warp
