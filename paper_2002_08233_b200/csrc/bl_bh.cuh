@@ -821,7 +821,9 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
       // parallel over all warps (no warp waits before its items are done).
       const unsigned stamp = (unsigned)batches + 1u;
       bh_attr_items(p, lo, lo + bt, gw, GW, stamp, plo, phi, pend_prev);
-      for (int i = gw; i < bt; i += GW) {
+      // batch entry i -> CTA i mod G, warp i / G: the queries spread over
+      // all SMs (b = 1024 on 148 SMs: ~7 concurrent traversals per SM)
+      for (int i = warp * G + c; i < bt; i += GW) {
         const int v = lo + i;
         const float2 cv = __ldcg(p.xy + v);
         const float2 f = bh_force_warp(p, sh, v, cv, plo, phi, pend_prev, stamp, vis);
