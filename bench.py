@@ -265,10 +265,11 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
 
     # ---- e2e through the host C-ABI call (H2D + kernel + D2H inside bl_layout)
     e2e_steps = max(1, min(args.steps, 3))
-    h_xy = torch.from_numpy(xy0.copy()).pin_memory().numpy()
+    pinned = torch.empty(xy0.shape, dtype=torch.float32).pin_memory()   # page-locked inputs
+    buf = pinned.numpy()
     tot = 0.0
     for _ in range(e2e_steps):
-        buf = h_xy.copy()
+        np.copyto(buf, xy0)                                        # fresh inputs, untimed
         flush.fill_(0.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -291,7 +292,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(workload_desc(name, g, cfg), model={"a": args.a, "r": args.r},
+        "config": dict(workload_desc(name, g, cfg), energy_model={"a": args.a, "r": args.r},
                        l2="flushed (512 MiB write) before every timed step",
                        parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
         "iters_per_sec": world * args.steps * cfg.iters / t_max,
