@@ -187,6 +187,17 @@ def cpu_cores():
     return int(oracle.max_threads())
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------ main arms
 def bench_reference(args, name, g, xy0, cfg, rank, world):
     if rank != 0:
@@ -320,6 +331,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         b = min(cfg.batch, g.n)
         line["cpu_baseline"] = {
             "value": pairs / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+            "cpu_model": cpu_model(), "per_core": pairs / dt / max(1, cpu_cores()),
             "sample": f"first {k} batch update(s) of iteration 0 of {name} (b={b}), {dt:.1f} s",
         }
     if not args.no_bh:

@@ -405,3 +405,37 @@ def test_C6_million_vertices_one_batch():
     ref[:b] += f / np.hypot(f[:, 0], f[:, 1])[:, None]
     assert_positions_close(got, ref, what="C6 one batch")
     assert np.array_equal(got[b:], xy0[b:])
+
+
+_FUZZ = [  # (graph, n-ish, batch, K, C, flags) -- both drivers, staged and L2 targets
+    ("rmat", 11, 3000, 1.0, 1.0, 0),      # b > BL_TGT_CAP: targets read from L2, pipelined
+    ("rmat", 13, 2049, 0.7, 1.3, 0),      # odd b > cap: two-barrier driver
+    ("rmat", 12, 333, 1.0, 1.0, 1),       # odd b: two-barrier driver, REPULSE_NEIGHBORS
+    ("ba", 3000, 512, 1.5, 0.5, 0),
+    ("grid", 57, 1000, 1.0, 2.0, 0),      # ragged last batch
+    ("grid", 20, 400, 1.0, 1.0, 0),       # b = n: one batch per iteration
+    ("rmat", 9, 10, 1.0, 1.0, 0),         # tiny batches, many of them
+    ("ba", 700, 2, 1.0, 1.0, 1),
+]
+
+
+@pytest.mark.parametrize("case", _FUZZ)
+def test_fuzz_shapes_one_iteration(case):
+    """Random graph shapes x batch sizes that exercise both drivers (pipelined
+    needs b even, <= 2048 and >= 4 batches), L2-resident targets and ragged
+    tails: one iteration vs the oracle, energy within 1e-3."""
+    from blgen import ba_graph
+    kind, size, b, K, C, flags = case
+    if kind == "rmat":
+        g = rmat_graph(size, 8, 0.57, 0.19, 0.19, seed=size)
+    elif kind == "ba":
+        g = ba_graph(size, 2, seed=size)
+    else:
+        g = grid_graph(size, size + 3)
+    xy0 = uniform_coords(g.n, 100 + size)
+    p = dict(iters=1, batch=b, K=K, C=C, flags=flags)
+    got, tr, done = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert done == 1
+    assert_positions_close(got, ref, what=f"fuzz {case}")
+    assert abs(tr[0] - E[0]) <= 1e-3 * E[0]
