@@ -179,9 +179,12 @@ int32_t bl_max_vertices(void);
  * bl_forces call enqueued (the persistent design launches exactly one). */
 int32_t bl_last_launch_count(const bl_ctx *h);
 
-/* Name of the kernel variant h launches, "bl_layout_kernel<NT,T,TP>" (NT
- * threads per CTA, T register-blocked targets per thread, TP of them with
- * paired reciprocals).  Static storage owned by h. */
+/* Name of the kernel the last layout call on h launched -- the whole-GPU
+ * "bl_layout_kernel<NT,T,TP>" (NT threads per CTA, T register-blocked targets
+ * per thread, TP of them with paired reciprocals), the single-cluster
+ * "bl_cluster_kernel<T,TP> xCS" used for small graphs, or "bl_bh_kernel<512>"
+ * -- or, before any call, the whole-GPU variant.  Static
+ * storage owned by h. */
 const char *bl_kernel_name(const bl_ctx *h);
 
 /* Microbenchmark of the roofline denominators on the current device:

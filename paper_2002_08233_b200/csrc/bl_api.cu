@@ -19,6 +19,7 @@
 #include "bl_kernel.cuh"
 #include "bl_bh.cuh"
 #include "bl_metrics.cuh"
+#include "bl_cluster.cuh"
 
 #ifndef BL_DEFAULT_NT
 #define BL_DEFAULT_NT 512
@@ -65,6 +66,7 @@ struct bl_ctx {
   int32_t launches = 0;
   std::string err;
   char kname[64] = {0};
+  char kname_last[64] = {0};  // the kernel the last layout call launched
   // BatchLayoutBH scratch (allocated on first use, sized by n)
   bool bh_ready = false;
   unsigned *d_keyA = nullptr, *d_keyB = nullptr, *d_hist = nullptr;
@@ -147,7 +149,9 @@ extern "C" const char *bl_last_error(const bl_ctx *h) {
 
 extern "C" int32_t bl_last_launch_count(const bl_ctx *h) { return h ? h->launches : 0; }
 
-extern "C" const char *bl_kernel_name(const bl_ctx *h) { return h ? h->kname : ""; }
+extern "C" const char *bl_kernel_name(const bl_ctx *h) {
+  return h ? (h->kname_last[0] ? h->kname_last : h->kname) : "";
+}
 
 // Not part of the public header: phase profile of the last launch when the
 // context was created with BL_PROFILE=1 (debug aid for bench.py --prof).
@@ -582,6 +586,103 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   return BL_OK;
 }
 
+// Small graphs: the exact method on one thread-block cluster (bl_cluster.cuh)
+// when a batch's work is small enough that the whole-GPU kernel's per-batch
+// grid barrier dominates (b n <= BL_CLUSTER_PAIRS, default 1e6: measured
+// crossover ~1.5e6 pairs per batch on B200) and the
+// coordinates fit every CTA's shared memory.  Returns BL_OK and sets *used.
+static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
+                                bool *used) {
+  *used = false;
+  const int n = h->n, b = std::min(p->batch, n);
+  if (env_int("BL_CLUSTER", 1) == 0) return BL_OK;
+  const long long pairs_max = env_int("BL_CLUSTER_PAIRS", 1000000);
+  if ((long long)b * n > pairs_max) return BL_OK;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int n4 = (n + 1) / 2;
+  size_t smem = blc_smem_bytes(n4, b);
+  if (smem + 2048 > (size_t)optin) return BL_OK;
+  // the CSR too, when it fits (one L2 round trip less per row per batch)
+  const size_t csr_bytes = sizeof(int) * ((size_t)n + 1 + (size_t)h->nnz);
+  const bool csr_smem = smem + csr_bytes + 2048 <= (size_t)optin;
+  if (csr_smem) smem += csr_bytes;
+  int amode, rmode;
+  float a_half, r_half;
+  model_codes(p, &amode, &rmode, &a_half, &r_half);
+  // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
+  int CS = 0;
+  void *fns[3][2] = {{(void *)bl_cluster_kernel<1, 0>, (void *)bl_cluster_kernel<1, -1>},
+                     {(void *)bl_cluster_kernel<2, 0>, (void *)bl_cluster_kernel<2, -1>},
+                     {(void *)bl_cluster_kernel<4, 0>, (void *)bl_cluster_kernel<4, -1>}};
+  const int tsel = env_int("BL_CLUSTER_T", 0);  // 0: by slice size
+  for (int cs : {16, 8}) {
+    const int sl = (b + cs - 1) / cs;
+    if (sl > BLC_SLICE_MAX) continue;
+    const int tt = tsel == 1 ? 0 : tsel == 2 ? 1 : tsel == 4 ? 2 : (sl <= 16 ? 0 : 1);
+    void *kfn = fns[tt][rmode ? 1 : 0];
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      continue;
+    if (cs > 8 && cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      continue;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(BLC_NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) != cudaSuccess || nclusters < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    CS = cs;
+    bl_status s;
+    if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
+    BLCParams k{};
+    k.n = n;
+    k.b = b;
+    k.nb = (n + b - 1) / b;
+    k.iters = p->iters;
+    k.max_batches = p->max_batches;
+    k.flags = p->flags;
+    k.ck2 = p->C * p->K * p->K;
+    k.invK = 1.0f / p->K;
+    k.step0 = p->step0;
+    k.cooling = p->cooling;
+    k.tol = p->tol;
+    k.amode = amode;
+    k.rmode = rmode;
+    k.a_half = a_half;
+    k.r_half = r_half;
+    k.n4 = n4;
+    k.nnz = h->nnz;
+    k.csr_smem = csr_smem ? 1 : 0;
+    k.xy = d_xy;
+    k.rowptr = h->d_rowptr;
+    k.colidx = h->d_colidx;
+    k.energy = h->d_energy;
+    k.iters_done = h->d_iters_done;
+    BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+    void *args[] = {&k};
+    BL_CUDA(h, cudaLaunchKernelExC(&cfg, kfn, args));
+    h->launches = 1;
+    snprintf(h->kname_last, sizeof h->kname_last, "bl_cluster_kernel<%d,%d> x%d", 1 << tt,
+             rmode ? -1 : 0, CS);
+    *used = true;
+    return BL_OK;
+  }
+  (void)CS;
+  return BL_OK;
+}
+
 extern "C" bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits) {
   if (!h || !visits) return fail(h, BL_EINVAL, "NULL argument");
   *visits = 0;
@@ -609,8 +710,15 @@ extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p
     return BL_OK;
   }
   h->last_bh = false;
-  s = p->algo == BL_ALGO_BH ? launch_bh(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr)
-                            : launch(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr);
+  snprintf(h->kname_last, sizeof h->kname_last, "%s", p->algo == BL_ALGO_BH ? "bl_bh_kernel<512>" : h->kname);
+  bool clustered = false;
+  if (p->algo == BL_ALGO_EXACT) {
+    s = launch_cluster(h, reinterpret_cast<float2 *>(d_xy), p, st, &clustered);
+    if (s != BL_OK) return s;
+  }
+  if (!clustered)
+    s = p->algo == BL_ALGO_BH ? launch_bh(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr)
+                              : launch(h, reinterpret_cast<float2 *>(d_xy), p, st, 0, 0, 0, nullptr);
   if (s != BL_OK) return s;
   h->have_layout = true;
   return BL_OK;

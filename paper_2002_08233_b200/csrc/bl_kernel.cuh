@@ -238,8 +238,8 @@ __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0
 // f_a(d)/d = d^(a-1)/K plus, in the if/else model, the removal of the
 // all-pairs repulsion rep * d^(r-1) (rep = C K^2, or 0 with
 // BL_REPULSE_NEIGHBORS).  rs = 1/d.
-template <bool FAST>
-__device__ __forceinline__ float bl_model_coef(const BLKParams &p, float d2, float rs, float rep) {
+template <bool FAST, class P>
+__device__ __forceinline__ float bl_model_coef(const P &p, float d2, float rs, float rep) {
   if (FAST) return fmaf(rep * rs, rs, d2 * rs * p.invK);  // (a, r) = (2, -1)
   float at;
   switch (p.amode) {
