@@ -201,6 +201,7 @@ static const BLVariant kVariants[] = {
     BL_V(768, 6, 2),  BL_V(768, 4, 1),  BL_V(768, 4, 2),
     BL_V(1024, 4, 1), BL_V(1024, 4, 2), BL_V(1024, 2, 1),
     BL_V(512, 8, -1),  // general repulsion exponent r (reading C15)
+    BL_V(256, 16, 6),  // 8 warps x 16 targets: best at 2^20 vertices (0.92), not at C5
 };
 #undef BL_V
 static const BLVariant *find_variant(int NT, int T, int TP) {
