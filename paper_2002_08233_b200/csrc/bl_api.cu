@@ -464,8 +464,14 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.guided = env_int("BL_GUIDED", 2);
   model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
-  const BLVariant *vt = k.rmode == 0 ? find_variant(h->NT, h->T, h->TP) : find_variant(512, 8, -1);
+  // very large batches (b n >= 5e8 pairs, e.g. 2^20 vertices x 1024) amortise
+  // the fewer, wider warps of <256,16,6> best; below, <512,8,2> (measured)
+  const bool wide = !getenv("BL_NT") && (long long)b * n >= 500000000LL;
+  const BLVariant *vt = k.rmode != 0 ? find_variant(512, 8, -1)
+                        : wide       ? find_variant(256, 16, 6)
+                                     : find_variant(h->NT, h->T, h->TP);
   void *kfn = vt->fn;
+  snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
   int occ = 0;
