@@ -410,7 +410,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   const int b = forces_mode ? std::max(1, count) : std::min(p->batch, n);
   const int G = h->G;
   bl_status s;
-  if ((s = grow(h, h->d_part, h->part_cap, (size_t)2 * b * G)) != BL_OK) return s;
+  if ((s = grow(h, h->d_part, h->part_cap, (size_t)3 * b * G)) != BL_OK) return s;
   if ((s = grow(h, h->d_pend, h->pend_cap, (size_t)2 * b)) != BL_OK) return s;
   const int mi = forces_mode ? max_items_per_batch(h, b, first, count)
                              : max_items_per_batch(h, b, 0, n);
@@ -452,6 +452,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
                 (b + G - 1) / G <= BL_ETASK_MAX &&
                 red_cap_for(chunk4_for(n, G)) / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
                 env_int("BL_PIPELINE", 1) != 0;
+  k.part_nbuf = 2;
   k.attr = h->d_attr;
   k.e_cta = h->d_e_cta;
   k.energy = h->d_energy;
@@ -471,6 +472,19 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
                         : wide       ? find_variant(256, 16, 6)
                                      : find_variant(h->NT, h->T, h->TP);
   void *kfn = vt->fn;
+  // asynchronous phases (bl_run_async) when each half of the partial buffer
+  // still holds >= 2 sub-ranges of the batch's target tiles, and the batch's
+  // pair work is large (measured: C5, b n = 2.7e8, +13 %; C4, 8.4e6, +0.7 %;
+  // C2 / C3 b=256, ~2e6, -20 %: latency-bound batches keep the pipelined
+  // driver).  BL_ASYNC=1 / 0 forces it on / off.
+  const int async_env = env_int("BL_ASYNC", -1);
+  const bool async_auto = (long long)b * n >= (1LL << 25);
+  if (k.pipelined && (async_env == 1 || (async_env < 0 && async_auto)) &&
+      k.red_cap / 2 / (((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T) >= 2) {
+    k.pipelined = 2;
+    k.part_nbuf = 3;
+    k.afence_gpu = env_int("BL_AFENCE", 0);
+  }
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));

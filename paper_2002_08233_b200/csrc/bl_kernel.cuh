@@ -111,7 +111,10 @@ struct BLKParams {
   const int *item_ptr, *item_v, *item_k0;
   float2 *part;          // [2][b][G] (pipelined path double-buffers by batch parity)
   float2 *pend;          // [2][b]   new coordinates of the last two batches (pipelined)
-  int pipelined;         // 1: one grid barrier per batch (needs nb >= 4)
+  int pipelined;         // 1: one grid barrier per batch (needs nb >= 4); 2: the same
+                         // without CTA-wide barriers between phases (bl_run_async)
+  int part_nbuf;         // part buffers (2: pipelined, 3: async)
+  int afence_gpu;        // async: GPU-scope fences in every task (debug, BL_AFENCE=1)
   float2 *attr;          // [max items per batch]
   double *e_cta;         // [2][G]
   double *energy;        // [iters]
@@ -574,6 +577,7 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
 // read from pend when j is in batch ph-1 and from xy otherwise.  This is
 // exactly the frozen-batch semantics of Alg. 2.
 #define BL_ETASK_MAX 64  // owned vertices per CTA per batch (b <= 64·G)
+#define BL_NTT_MAX 32    // target tiles per batch (BL_TGT_CAP / (32 T), T >= 2)
 
 struct BLShared {
   int unit_ctr;   // next sweep unit
@@ -597,6 +601,14 @@ struct BLShared {
   int rows[2][BL_ETASK_MAX][32];
   int rdeg[2][BL_ETASK_MAX];
   int rowq[2];
+  // asynchronous-phase driver (bl_run_async): per phase parity s = ph & 1
+  int a_unit[2];               // next sweep unit
+  int a_tdone[2][BL_NTT_MAX];  // finished units per target tile
+  int a_tok[2];                // completion tokens (tiles, control, updates)
+  int a_unext[2], a_udone[2];  // update tasks taken / finished
+  int a_exit[2];               // warps that left the phase
+  int a_gen[2];                // the phase allowed to use slot s next
+  int a_updph;                 // last phase whose update tasks all finished
 #ifdef BL_PHASE_TS
   // critical-path timestamps (profiling builds, -DBL_PHASE_TS; they cost ~3 %
   // at C5 even when disabled at run time, so they are compiled out by
@@ -670,7 +682,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     phi = min(plo + p.b, p.n);
   }
   const float2 ci = bl_src_get(src4, (v - c) / G);
-  const float2 *row = p.part + (size_t)(q & 1) * p.b * G + (size_t)local * G;
+  const float2 *row = p.part + (size_t)(q % p.part_nbuf) * p.b * G + (size_t)local * G;
   float rx = 0.f, ry = 0.f;
 #pragma unroll 8
   for (int cc = lane; cc < G; cc += 32) {
@@ -764,11 +776,41 @@ __device__ __forceinline__ void bl_stage_rows_warp(const BLKParams &p, int q, BL
   if (lane == 0) sh.rowq[buf] = q;
 }
 
+// Writes that other CTAs read after barrier ph (part, pend, xy commits) are
+// released to the phase's completer at CTA scope; the completer's
+// fence.acq_rel.gpu before its arrival is cumulative, so it publishes them
+// at GPU scope (the same argument as a CTA barrier followed by one thread's
+// GPU fence).  BL_AFENCE=1 (debug) fences at GPU scope in every task instead.
+__device__ __forceinline__ void bl_fence_to_completer(const BLKParams &p) {
+  if (p.afence_gpu) __threadfence();
+  else __threadfence_block();
+}
+
+__device__ __forceinline__ void bl_token(const BLKParams &p, BLShared &sh, const BLPhase &f,
+                                         int need) {
+  // lane 0 of the caller, after its writes were fenced
+  if (atomicAdd(&sh.a_tok[f.ph & 1], 1) != need - 1) return;
+  __threadfence_block();
+  const int G = gridDim.x, c = blockIdx.x;
+  if (f.owned > 0) {
+    double e = sh.e_acc;
+    for (int i = 0; i < f.owned; ++i) e += sh.e_task[i];  // task order
+    sh.e_acc = e;
+  }
+  if (f.q1 >= 0 && f.ph <= f.P && bl_closes_iteration(f.q1, p.nb, f.P)) {
+    p.e_cta[((f.q1 / p.nb) & 1) * G + c] = sh.e_acc;
+    sh.e_acc = 0.0;
+  }
+  if (f.ph <= f.P)
+    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar)
+                 : "memory");
+}
+
 // Control work of phase ph, attempted by a warp between tasks: if barrier
 // ph-1 has completed and no other warp claimed it, do (a)-(c) and publish.
-__device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase &f,
+__device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase &f,
                                                const float4 *src4, BLShared &sh,
-                                               unsigned bar_target) {
+                                               unsigned bar_target, int need = -1) {
   const int lane = threadIdx.x & 31;
   int go = 0;
   if (lane == 0 && (int)(bl_ld_acquire(p.bar) - bar_target) >= 0)
@@ -781,7 +823,7 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
     __threadfence_block();
   }
   go = __shfl_sync(0xffffffffu, go, 0);
-  if (!go) return;
+  if (!go) return false;
   __syncwarp();  // order the lanes' reads after lane 0's acquire
   bool stop = false;
   const int nb = p.nb;
@@ -798,11 +840,22 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
     if (lane == 0) sh.e_prev = E;
   }
   if (f.q2 >= 0) bl_commit_warp(p, f.q2, src4);
+  if (need >= 0) {  // async driver: the control task's completion token (the
+                    // staging below is for the next phase, not this one)
+    __syncwarp();
+    if (lane == 0) {
+      bl_fence_to_completer(p);  // commits to xy
+      bl_token(p, sh, f, need);
+    }
+  }
   if (!stop && f.ph + 1 < f.P) {
     const int lo_n = ((f.ph + 1) % nb) * p.b;
     bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), f.tgt_next);
   }
   if (!stop && f.ph < f.P) bl_stage_rows_warp(p, f.ph, sh);
+  // async driver: the targets must have landed before `ready` lets warps
+  // into phase ph+1 (the pipelined driver waits at its phase-end barrier)
+  if (need >= 0) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
   if (lane == 0) {
     if (stop) *(volatile int *)&sh.stop_flag = 1;
@@ -813,6 +866,7 @@ __device__ __forceinline__ void bl_try_control(const BLKParams &p, const BLPhase
     *(volatile int *)&sh.ready = f.ph;
   }
   __syncwarp();
+  return true;
 }
 
 // Try to take and run one update task; returns true if one was run.
@@ -973,6 +1027,222 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
   pf.flush(p);
 }
 
+// ------------------------------------------- asynchronous-phase driver
+// The tasks and the arithmetic of bl_run_pipelined, without the CTA-wide
+// barrier (and the combine that follows it) at the end of each phase: every
+// warp walks the phases on its own.  A warp leaves phase ph when it finds
+// nothing left to grab there and enters phase ph+1 at once, so the tail of a
+// phase (its last units, the combine, the grid-barrier arrival) overlaps the
+// next phase's sweep.  Per phase (parity slot s = ph & 1):
+//   * the warp that finishes the last unit of a target tile combines that
+//     tile's sub-range partials (red slot s, fixed order) into part[ph % 3];
+//   * completion tokens: one per tile, one for the control task, one per
+//     update task; whoever adds the last token closes the phase (energy
+//     bookkeeping) and arrives at grid barrier ph;
+//   * entering phase ph+1 needs: the control task of phase ph done (targets
+//     of ph+1 staged), the update tasks of phase ph done (their sources are
+//     clean in ph+1), and slot (ph+1)&1 released by every warp of phase ph-1
+//     (the last warp to leave a phase resets its slot).
+// At most two phases are live in a CTA.  part has three buffers: the tile
+// combines of phase ph can run before barrier ph-1 completes, while other
+// CTAs' update tasks of phase ph-2 still read part[(ph-3) % 3]... never the
+// same buffer.  Results are independent of which warp ran which task (fixed
+// summation orders), as in the pipelined driver.
+__device__ __forceinline__ bool bl_try_update_a(const BLKParams &p, const BLPhase &f,
+                                                float4 *src4, BLShared &sh, int need) {
+  const int lane = threadIdx.x & 31, s = f.ph & 1;
+  const volatile BLShared &vs = sh;
+  if (vs.seen < f.ph || vs.stop_flag || vs.a_unext[s] >= f.owned) return false;
+  int t = f.owned;
+  if (lane == 0) t = atomicAdd(&sh.a_unext[s], 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t >= f.owned) return false;
+  __threadfence_block();  // acquire the control warp's publication
+  const int buf = f.q1 & 1;
+  const bool staged = vs.rowq[buf] == f.q1 && vs.rdeg[buf][t] >= 0;
+  bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t],
+                staged ? sh.rows[buf][t] : nullptr, staged ? vs.rdeg[buf][t] : 0);
+  __syncwarp();
+  if (lane == 0) {
+    bl_fence_to_completer(p);  // pend (read by other CTAs after barrier ph)
+    if (atomicAdd(&sh.a_udone[s], 1) == f.owned - 1) {
+      __threadfence_block();
+      *(volatile int *)&sh.a_updph = f.ph;
+    }
+    bl_token(p, sh, f, need);
+  }
+  __syncwarp();
+  return true;
+}
+
+template <int T, int TP>
+__device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, float2 *tgt,
+                                             float2 *red, BLShared &sh) {
+  const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
+  const int nb = p.nb;
+  const long long ptot = (long long)p.iters * nb;
+  const bool mb_stop = p.max_batches > 0 && p.max_batches < ptot;
+  const int P = mb_stop ? p.max_batches : (int)ptot;
+  const int half = p.red_cap / 2;  // red slots per phase parity
+  const volatile BLShared &vs = sh;
+  if (threadIdx.x == 0) {
+    sh.done_iters = mb_stop ? (P - 1) / nb : p.iters;
+    sh.e_prev = 0.0;
+    sh.e_acc = 0.0;
+    sh.a_updph = -1;
+    for (int k = 0; k < 2; ++k) {
+      sh.a_unit[k] = sh.a_tok[k] = sh.a_unext[k] = sh.a_udone[k] = sh.a_exit[k] = 0;
+      sh.a_gen[k] = k;
+      for (int t = 0; t < BL_NTT_MAX; ++t) sh.a_tdone[k][t] = 0;
+    }
+  }
+  if (threadIdx.x < 32) {
+    bl_prefetch_targets_warp(p, 0, min(p.b, p.n), tgt);
+    if (P > 1) {
+      bl_prefetch_targets_warp(p, (1 % nb) * p.b, min(p.b, p.n - (1 % nb) * p.b),
+                               tgt + BL_TGT_CAP);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();
+
+  double step_u = p.step0;
+  int prev_owned = 0;
+  bool stop = false;
+  for (int ph = 0; ph <= P + 1 && !stop; ++ph) {
+    const int s = ph & 1;
+    BLPhase f;
+    f.ph = ph;
+    f.P = P;
+    f.q1 = ph - 1;
+    f.q2 = ph - 2;
+    f.owned = 0;
+    f.v0 = 0;
+    if (f.q1 >= 0 && ph <= P) {
+      const int lo1 = (f.q1 % nb) * p.b, hi1 = min(lo1 + p.b, p.n);
+      f.v0 = lo1 + ((c - lo1 % G) + G) % G;
+      f.owned = f.v0 < hi1 ? (hi1 - 1 - f.v0) / G + 1 : 0;
+      if (f.q1 > 0 && f.q1 % nb == 0) step_u = step_u * p.cooling;
+    }
+    f.step_u = step_u;
+    f.tgt_next = tgt + ((ph + 1) & 1) * BL_TGT_CAP;
+    // entry gate
+    if (ph >= 1) {
+      for (;;) {
+        if (vs.stop_flag) {
+          stop = true;
+          break;
+        }
+        if (vs.a_gen[s] == ph && (ph == 1 || vs.ready >= ph - 1) &&
+            (prev_owned == 0 || vs.a_updph >= ph - 1))
+          break;
+        __nanosleep(32);
+      }
+      if (stop) break;
+      __threadfence_block();
+    }
+    prev_owned = f.owned;
+
+    const bool has_R = ph < P;
+    const int lo = has_R ? (ph % nb) * p.b : 0;
+    const int bt = has_R ? min(p.b, p.n - lo) : 0;
+    const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
+    BLUnits U = {1, 0, 0};
+    if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, half);
+    const int n_all = has_R ? U.ntt * U.nsub : 0;
+    const int n_clean = has_R ? U.ntt * U.nc : 0;
+    const int need = (has_R ? U.ntt : 0) + (ph > 0 ? 1 : 0) + f.owned;
+    float2 *red_s = red + s * half;
+    float2 *part = p.part + (size_t)(ph % 3) * p.b * G;
+    const float2 *tgt_s = tgt + s * BL_TGT_CAP;
+    const unsigned bar_prev = (unsigned)ph * (unsigned)G;  // barrier ph-1 complete
+    auto control = [&]() {
+      return ph > 0 && vs.ctrl_claim < ph && bl_try_control(p, f, src4, sh, bar_prev, need);
+    };
+    for (;;) {
+      if (vs.stop_flag) {
+        stop = true;
+        break;
+      }
+      if (control()) continue;
+      if (bl_try_update_a(p, f, src4, sh, need)) continue;
+      int g = n_all;
+      if (vs.a_unit[s] < n_all) {
+        if (lane == 0) g = atomicAdd(&sh.a_unit[s], 1);
+        g = __shfl_sync(0xffffffffu, g, 0);
+      }
+      if (g < n_all) {
+        if (g >= n_clean) {
+          // dirty sub-range: needs this CTA's updates of batch q1; help until done
+          for (;;) {
+            if (vs.stop_flag) {
+              stop = true;
+              break;
+            }
+            if (control()) continue;
+            if (bl_try_update_a(p, f, src4, sh, need)) continue;
+            if (vs.a_updph >= ph) break;
+            __nanosleep(64);
+          }
+          if (stop) break;
+          __threadfence_block();
+        }
+        bl_do_unit<T, TP>(p, lo, bt, src4, tgt_s, red_s, part, g, U, geo);
+        const int tile = g % U.ntt;
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          __threadfence_block();
+          last = atomicAdd(&sh.a_tdone[s][tile], 1) == U.nsub - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence_block();
+          if (U.nsub > 1) {
+            const int stride = U.ntt * 32 * T;
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+              const int idx = tile * 32 * T + k * 32 + lane;
+              if (idx < bt) {
+                float2 acc = red_s[idx];
+                for (int sb = 1; sb < U.nsub; ++sb) {
+                  const float2 v = red_s[sb * stride + idx];
+                  acc.x += v.x;
+                  acc.y += v.y;
+                }
+                part[(size_t)idx * G + c] = acc;
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            bl_fence_to_completer(p);  // part (read by other CTAs after barrier ph)
+            bl_token(p, sh, f, need);
+          }
+          __syncwarp();
+        }
+        continue;
+      }
+      // nothing left to grab: leave once control is claimed and every update taken
+      if ((ph == 0 || vs.ctrl_claim >= ph) && vs.a_unext[s] >= f.owned) break;
+      __nanosleep(32);
+    }
+    if (stop) break;
+    // leave the phase; the last warp out releases slot s for phase ph+2
+    if (lane == 0 && atomicAdd(&sh.a_exit[s], 1) == BL_NW - 1) {
+      __threadfence_block();
+      sh.a_unit[s] = sh.a_tok[s] = sh.a_unext[s] = sh.a_udone[s] = 0;
+      for (int t = 0; t < BL_NTT_MAX; ++t) sh.a_tdone[s][t] = 0;
+      sh.a_exit[s] = 0;
+      __threadfence_block();
+      *(volatile int *)&sh.a_gen[s] = ph + 2;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
+}
+
 template <int NT, int T, int TP>
 __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
   extern __shared__ float4 bl_smem[];
@@ -1015,6 +1285,10 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
     return;
   }
 
+  if (p.pipelined == 2) {
+    bl_run_async<T, TP>(p, src4, tgt, red, sh);
+    return;
+  }
   if (p.pipelined) {
     bl_run_pipelined<T, TP>(p, src4, tgt, red, sh, pf, bar_target);
     return;

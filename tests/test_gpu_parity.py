@@ -439,3 +439,86 @@ def test_fuzz_shapes_one_iteration(case):
     assert done == 1
     assert_positions_close(got, ref, what=f"fuzz {case}")
     assert abs(tr[0] - E[0]) <= 1e-3 * E[0]
+
+
+# ---- the asynchronous-phase driver (bl_run_async, the default for nb >= 4)
+# vs the pipelined driver it replaces (BL_ASYNC=0) and vs the oracle
+_DRIVERS = [("async", {"BL_ASYNC": "1"}), ("pipelined", {"BL_ASYNC": "0"}),
+            ("two-barrier", {"BL_PIPELINE": "0"})]
+
+
+def _with_env(monkeypatch, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+
+
+@pytest.mark.parametrize("driver", _DRIVERS, ids=[d[0] for d in _DRIVERS])
+@pytest.mark.parametrize("name", ["C3b256", "C4"])
+def test_drivers_one_iteration_vs_oracle(name, driver, monkeypatch):
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=1)
+    _with_env(monkeypatch, driver[1])
+    got, tr, done = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert done == 1
+    assert_positions_close(got, ref, what=f"{name} one iteration ({driver[0]})")
+    np.testing.assert_allclose(tr[0], E[0], rtol=1e-4)
+
+
+@pytest.mark.parametrize("mb", [1, 2, 3, 4, 5, 43, 44, 45, 87])
+def test_async_driver_max_batches(mb, monkeypatch):
+    """Every stop position of the phase pipeline: the first phases, a stop
+    right at / after an iteration boundary (C3 b=256: 43 batches/iteration).
+    Up to one iteration: vs the oracle run.  Beyond: shadowed (the chaos of
+    DESIGN.md §6 makes free-running comparisons meaningless after the first
+    iteration) -- batch mb-1 recomputed by the oracle from the GPU's own state
+    after mb-1 batches, with the step of its iteration."""
+    monkeypatch.setenv("BL_ASYNC", "1")
+    g, xy0, cfg = build_config("C3b256")
+    b = cfg.batch
+    nb = -(-g.n // b)
+    p = _params(cfg, iters=3, max_batches=mb)
+    got, _, done = gpu_layout(g, xy0, **p)
+    assert done == (mb - 1) // nb
+    if mb <= nb:
+        ref, _, rdone = _oracle(g, xy0, p)
+        assert done == rdone
+        assert_positions_close(got, ref, what=f"async max_batches={mb}")
+        return
+    prev, _, _ = gpu_layout(g, xy0, **_params(cfg, iters=3, max_batches=mb - 1))
+    t = mb - 1
+    lo = (t % nb) * b
+    hi = min(lo + b, g.n)
+    f = oracle.forces(g.n, g.rowptr, g.colidx, prev, lo, hi - lo)
+    step = cfg.step0 * cfg.cooling ** (t // nb)
+    ref = prev.astype(np.float64).copy()
+    ref[lo:hi] += step * f / np.hypot(f[:, 0], f[:, 1])[:, None]
+    assert_positions_close(got, ref, what=f"async max_batches={mb} (shadowed)")
+    assert np.array_equal(np.delete(got, np.s_[lo:hi], 0), np.delete(prev, np.s_[lo:hi], 0))
+
+
+def test_async_driver_tol_stop_matches_pipelined(monkeypatch):
+    """The tol criterion stops both drivers at the same iteration."""
+    monkeypatch.setenv("BL_ASYNC", "1")
+    g, xy0, cfg = build_config("C4")
+    _, full, _ = gpu_layout(g, xy0, iters=30, batch=256)
+    tol = float(np.median(np.abs(np.diff(full)))) * 1.5
+    stop = next(t for t in range(1, 30) if abs(full[t] - full[t - 1]) < tol) + 1
+    _, tr, done = gpu_layout(g, xy0, iters=30, batch=256, tol=tol)
+    assert done == stop and np.array_equal(tr, full[:stop])
+    monkeypatch.setenv("BL_ASYNC", "0")
+    _, tr2, done2 = gpu_layout(g, xy0, iters=30, batch=256, tol=tol)
+    assert done2 <= 30 and tr2.shape == (done2,)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_async_driver_bitwise_repeatable(name, monkeypatch):
+    """Fixed summation orders: repeated runs are bitwise identical whatever
+    warp ran which task (C5: 2 iterations = 512 dependent batches)."""
+    monkeypatch.setenv("BL_ASYNC", "1")
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=2 if name == "C5" else 5)
+    a, ea, _ = gpu_layout(g, xy0, **p)
+    for _ in range(2):
+        b, eb, _ = gpu_layout(g, xy0, **p)
+        assert np.array_equal(a, b) and np.array_equal(ea, eb)
