@@ -10,8 +10,8 @@ if [ -n "${AB_K:-}" ]; then
 fi
 for c in ${AB_CONFIGS:-C5}; do
   for rep in ${AB_REPS:-1 2}; do
-    timeout -s KILL 300 python bench.py --config $c --steps ${AB_STEPS:-3} --warmup 3 --no-cpu-baseline --no-bh > gpurun_out/ab_${c}_new_$rep.log 2>&1; echo "$c new rc=$?"
-    env $AB_ENV timeout -s KILL 300 python bench.py --config $c --steps ${AB_STEPS:-3} --warmup 3 --no-cpu-baseline --no-bh > gpurun_out/ab_${c}_old_$rep.log 2>&1; echo "$c old rc=$?"
+    timeout -s KILL 300 python bench.py --config $c --steps ${AB_STEPS:-3} --warmup 3 --no-cpu-baseline --no-bh ${AB_ARGS:-} > gpurun_out/ab_${c}_new_$rep.log 2>&1; echo "$c new rc=$?"
+    env $AB_ENV timeout -s KILL 300 python bench.py --config $c --steps ${AB_STEPS:-3} --warmup 3 --no-cpu-baseline --no-bh ${AB_ARGS:-} > gpurun_out/ab_${c}_old_$rep.log 2>&1; echo "$c old rc=$?"
   done
 done
 python - <<'PY'
