@@ -313,6 +313,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
             "traffic_source": traffic_src,
             "kernel": kname + " (persistent, cooperative; NT threads, T targets/thread, TP of them "
                               "paired-reciprocal)",
+            "driver": bl.bl_driver_name(lay.h),
             "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU/clk x {sm_max:.0f} MHz "
                           f"(sm_max_mhz, {peak_src}) / {mufu_per_pair} MUFU per pair",
             "frac_at_median_clock": (achieved * mufu_per_pair

@@ -187,6 +187,13 @@ int32_t bl_last_launch_count(const bl_ctx *h);
  * storage owned by h. */
 const char *bl_kernel_name(const bl_ctx *h);
 
+/* How the last layout call on h sequenced its dependent batches (DESIGN.md
+ * §4): "async" (one grid barrier per batch, no CTA-wide barrier between
+ * phases; b n >= 2^25), "pipelined" (one grid barrier per batch), "two-barrier"
+ * (phase R; barrier; phase U; barrier), "cluster" (single thread-block cluster)
+ * or "bh" (BatchLayoutBH); "" before any call.  Static storage owned by h. */
+const char *bl_driver_name(const bl_ctx *h);
+
 /* Microbenchmark of the roofline denominators on the current device:
  * sustained thread-op rates per SM per clock of (0) 3-register FFMA,
  * (1) MUFU.RCP (rcp.approx.ftz.f32), (2) MUFU.RSQ, (3) packed FFMA2

@@ -77,6 +77,8 @@ def _load() -> ctypes.CDLL:
     lib.bl_last_visits.restype = ctypes.c_int
     lib.bl_kernel_name.argtypes = [vp]
     lib.bl_kernel_name.restype = ctypes.c_char_p
+    lib.bl_driver_name.argtypes = [vp]
+    lib.bl_driver_name.restype = ctypes.c_char_p
     lib.bl_microbench.argtypes = [P(ctypes.c_double)]
     lib.bl_microbench.restype = ctypes.c_int
     lib.bl_debug_profile.argtypes = [vp, vp, i32]
@@ -94,7 +96,7 @@ lib = _load()
 
 # symbols include/bl.h declares (checked by tests/test_abi.py)
 EXPORTS = ("bl_params_default", "bl_greedy_init", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
-           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_edge_uniformity",
+           "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_driver_name", "bl_edge_uniformity",
            "bl_stress", "bl_neighborhood_preservation", "bl_microbench",
            "bl_debug_profile", "bl_destroy", "bl_status_string", "bl_last_error")
 
@@ -232,6 +234,10 @@ def bl_last_visits(h: int) -> int:
 
 def bl_kernel_name(h: int) -> str:
     return lib.bl_kernel_name(h).decode()
+
+
+def bl_driver_name(h: int) -> str:
+    return lib.bl_driver_name(h).decode()
 
 
 def bl_microbench():

@@ -67,6 +67,7 @@ struct bl_ctx {
   std::string err;
   char kname[64] = {0};
   char kname_last[64] = {0};  // the kernel the last layout call launched
+  const char *driver_last = "";  // its batch sequencing (bl_driver_name)
   // BatchLayoutBH scratch (allocated on first use, sized by n)
   bool bh_ready = false;
   unsigned *d_keyA = nullptr, *d_keyB = nullptr, *d_hist = nullptr;
@@ -148,6 +149,8 @@ extern "C" const char *bl_last_error(const bl_ctx *h) {
 }
 
 extern "C" int32_t bl_last_launch_count(const bl_ctx *h) { return h ? h->launches : 0; }
+
+extern "C" const char *bl_driver_name(const bl_ctx *h) { return h ? h->driver_last : ""; }
 
 extern "C" const char *bl_kernel_name(const bl_ctx *h) {
   return h ? (h->kname_last[0] ? h->kname_last : h->kname) : "";
@@ -486,6 +489,10 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     k.afence_gpu = env_int("BL_AFENCE", 0);
   }
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
+  h->driver_last = forces_mode ? "two-barrier"
+                   : k.pipelined == 2 ? "async"
+                   : k.pipelined      ? "pipelined"
+                                      : "two-barrier";
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
   int occ = 0;
@@ -697,6 +704,7 @@ static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
     h->launches = 1;
     snprintf(h->kname_last, sizeof h->kname_last, "bl_cluster_kernel<%d,%d> x%d", 1 << tt,
              rmode ? -1 : 0, CS);
+    h->driver_last = "cluster";
     *used = true;
     return BL_OK;
   }
@@ -732,6 +740,7 @@ extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p
   }
   h->last_bh = false;
   snprintf(h->kname_last, sizeof h->kname_last, "%s", p->algo == BL_ALGO_BH ? "bl_bh_kernel<512>" : h->kname);
+  h->driver_last = p->algo == BL_ALGO_BH ? "bh" : "";
   bool clustered = false;
   if (p->algo == BL_ALGO_EXACT) {
     s = launch_cluster(h, reinterpret_cast<float2 *>(d_xy), p, st, &clustered);

@@ -522,3 +522,21 @@ def test_async_driver_bitwise_repeatable(name, monkeypatch):
     for _ in range(2):
         b, eb, _ = gpu_layout(g, xy0, **p)
         assert np.array_equal(a, b) and np.array_equal(ea, eb)
+
+
+@pytest.mark.parametrize("env,expect", [({}, "async"), ({"BL_ASYNC": "0"}, "pipelined"),
+                                        ({"BL_PIPELINE": "0"}, "two-barrier")])
+def test_driver_selection_C5(env, expect, monkeypatch):
+    """C5 (b n = 2.7e8 >= 2^25) runs the asynchronous-phase driver by default;
+    bl_driver_name reports what ran (one batch)."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    _with_env(monkeypatch, env)
+    g, xy0, cfg = build_config("C5")
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=1, batch=cfg.batch, max_batches=1)
+        torch.cuda.synchronize()
+        assert bl.bl_driver_name(lay.h) == expect
+        assert bl.bl_kernel_name(lay.h) == "bl_layout_kernel<512,8,2>"
