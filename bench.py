@@ -337,6 +337,7 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         }
     if not args.no_bh:
         line["bh"] = bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, t_local / args.steps)
+    line["attraction"] = bench_attraction(lay, d_xy0, params, stream, flush, g, peaks)
     lay.close()
     if args.prof and rank == 0:
         line["phase_profile"] = phase_profile(g, xy0, params, dev, clocks.get("sm_mhz") or sm_max)
@@ -375,6 +376,44 @@ def bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, exact_s):
             "iters_per_sec": cfg.iters / t, "ms_per_step": 1e3 * t, "steps": steps,
             "visits_per_step": visits, "visits_per_sec": visits / t,
             "speedup_vs_exact": exact_s / t, "gpu_launches_per_step": bl.bl_last_launch_count(lay.h)}
+
+
+def bench_attraction(lay, d_xy0, params, stream, flush, g, peaks):
+    """Step a5 alone (bl_forces with BL_ATTRACTION_ONLY over all n vertices:
+    the CSR attraction + neighbour correction of one whole iteration, edge-
+    parallel items of <= 128 entries, one launch).  Algorithmic bytes: 4 B
+    colidx + 8 B gathered coordinate per CSR entry, rowptr, own coordinate
+    read + S_i write.  In the layout these gathers hit L2 (CSR + xy = 19 MB
+    at C5 stay resident), so `l2_warm` is the in-situ condition; `hbm_cold`
+    flushes L2 first."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    p = dict(params, flags=int(params.get("flags", 0)) | bl.BL_ATTRACTION_ONLY)
+    nbytes = 12 * g.nnz + 4 * (g.n + 1) + 16 * g.n
+    out = {}
+    for mode in ("l2_warm", "hbm_cold"):
+        lay.forces(d_xy0, 0, g.n, stream=stream, **p)
+        torch.cuda.synchronize()
+        ms = []
+        for i in range(5):
+            if mode == "hbm_cold":
+                flush.fill_(float(i))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            lay.forces(d_xy0, 0, g.n, stream=stream, **p)
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        t = float(np.median(ms)) / 1e3
+        out[mode] = {"us": 1e6 * t, "GB_per_s": nbytes / t / 1e9,
+                     "frac_of_hbm_peak": nbytes / t / 1e9 / float(peaks.get("hbm_gbs", 6540.2))}
+    out.update({"step": "a5 (CSR attraction + neighbour correction), all n vertices, one launch",
+                "algorithmic_bytes": nbytes, "csr_entries": int(g.nnz),
+                "kernel": bl.bl_kernel_name(lay.h) + " (forces mode, attraction only)",
+                "note": "latency-bound gathers (12 B per entry); in the layout the same code "
+                        "runs inside the update tasks, overlapped with the sweep"})
+    return out
 
 
 def phase_profile(g, xy0, params, dev, mhz):

@@ -39,7 +39,14 @@ enum {
    * Alg. 1 / Alg. 2 and the (i,j) not-in-E second
    * sum of §2.2.  With this flag adjacent pairs also repel (the
    * classic Fruchterman-Reingold form, and the BH variant Alg. S3). */
-  BL_REPULSE_NEIGHBORS = 1u << 0
+  BL_REPULSE_NEIGHBORS = 1u << 0,
+  /* bl_forces only (measurement / parity of step a5 alone): return the CSR
+   * attraction + neighbour correction S_i = sum over j in N(i) of
+   * (d^(a-1)/K + C K^2 d^(r-1)) Δ_ij (without the correction under
+   * BL_REPULSE_NEIGHBORS), i.e. f(i, c) without the all-pairs repulsion term
+   * -C K^2 R_i.  Rejected (BL_EINVAL) by bl_layout / bl_layout_device and
+   * with BL_ALGO_BH. */
+  BL_ATTRACTION_ONLY = 1u << 1
 };
 
 /* repulsion algorithm (bl_params.algo) */
@@ -67,7 +74,7 @@ typedef struct {
                           §4.5).  0 disables.                                  */
   int32_t max_batches; /* > 0: stop after that many batch updates in total
                           (debug / one-batch parity); <= 0: no limit           */
-  uint32_t flags;      /* BL_REPULSE_NEIGHBORS                                 */
+  uint32_t flags;      /* BL_REPULSE_NEIGHBORS; BL_ATTRACTION_ONLY (bl_forces)   */
   int32_t algo;        /* BL_ALGO_EXACT (default) or BL_ALGO_BH                */
   float theta;         /* BL_ALGO_BH: MAC threshold, accept a cell when
                           theta > D_cell / d; >= 0, 0 = exact; the

@@ -14,6 +14,7 @@ _SO = os.path.join(_HERE, "libbl.so")
 
 BL_OK, BL_EINVAL, BL_ENOMEM, BL_ECUDA, BL_ESTATE = 0, -1, -2, -3, -4
 BL_REPULSE_NEIGHBORS = 1
+BL_ATTRACTION_ONLY = 2
 BL_ALGO_EXACT, BL_ALGO_BH = 0, 1
 
 

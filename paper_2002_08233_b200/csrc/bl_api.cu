@@ -170,6 +170,11 @@ extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t 
 // out of the opt-in maximum before the dynamic buffers are sized
 static const int kStaticSmemReserve = (int)sizeof(BLShared) + 1024;
 
+static int env_int(const char *name, int def) {
+  const char *s = getenv(name);
+  return (s && *s) ? atoi(s) : def;
+}
+
 static int red_cap_for(int chunk4) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
@@ -177,7 +182,8 @@ static int red_cap_for(int chunk4) {
   const long long room =
       (long long)optin - 1024 - kStaticSmemReserve - (long long)bl_smem_bytes(chunk4, 0);
   long long cap = room / 8;
-  if (cap > BL_RED_MAX) cap = BL_RED_MAX;
+  const long long mx = env_int("BL_RED_CAP", BL_RED_MAX);  // tuning override
+  if (cap > mx) cap = mx;
   return (int)cap;
 }
 
@@ -186,10 +192,6 @@ static int chunk4_for(int n, int G) {
   return std::max(1, (per + 1) / 2);
 }
 
-static int env_int(const char *name, int def) {
-  const char *s = getenv(name);
-  return (s && *s) ? atoi(s) : def;
-}
 
 // Kernel variants (NT threads per CTA, T targets per thread, TP of them
 // paired-reciprocal).  NT x registers is one SM's register file: 512 x 128,
@@ -375,7 +377,10 @@ static bl_status check_params(bl_ctx *h, const bl_params *p) {
   if (!(p->step0 > 0.0) || !std::isfinite(p->step0)) return fail(h, BL_EINVAL, "step0 must be > 0");
   if (!(p->cooling > 0.0 && p->cooling <= 1.0)) return fail(h, BL_EINVAL, "cooling must be in (0,1]");
   if (!(p->tol >= 0.0) || !std::isfinite(p->tol)) return fail(h, BL_EINVAL, "tol must be >= 0");
-  if (p->flags & ~(uint32_t)BL_REPULSE_NEIGHBORS) return fail(h, BL_EINVAL, "unknown flags");
+  if (p->flags & ~(uint32_t)(BL_REPULSE_NEIGHBORS | BL_ATTRACTION_ONLY))
+    return fail(h, BL_EINVAL, "unknown flags");
+  if ((p->flags & BL_ATTRACTION_ONLY) && p->algo != BL_ALGO_EXACT)
+    return fail(h, BL_EINVAL, "BL_ATTRACTION_ONLY needs BL_ALGO_EXACT");
   if (p->algo != BL_ALGO_EXACT && p->algo != BL_ALGO_BH) return fail(h, BL_EINVAL, "unknown algo");
   if (p->algo == BL_ALGO_BH && (!(p->theta >= 0.f) || !std::isfinite(p->theta)))
     return fail(h, BL_EINVAL, "theta must be >= 0");
@@ -413,7 +418,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   const int b = forces_mode ? std::max(1, count) : std::min(p->batch, n);
   const int G = h->G;
   bl_status s;
-  if ((s = grow(h, h->d_part, h->part_cap, (size_t)3 * b * G)) != BL_OK) return s;
+  const bool attr_only = forces_mode && (p->flags & BL_ATTRACTION_ONLY);
+  if (!attr_only && (s = grow(h, h->d_part, h->part_cap, (size_t)3 * b * G)) != BL_OK) return s;
   if ((s = grow(h, h->d_pend, h->pend_cap, (size_t)2 * b)) != BL_OK) return s;
   const int mi = forces_mode ? max_items_per_batch(h, b, first, count)
                              : max_items_per_batch(h, b, 0, n);
@@ -438,6 +444,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.tol = p->tol;
   k.chunk4 = chunk4_for(n, G);
   k.forces_mode = forces_mode;
+  k.attr_only = attr_only ? 1 : 0;
   k.first = first;
   k.count = count;
   k.xy = d_xy;
@@ -502,6 +509,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
 
   BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+  if (h->d_prof) BL_CUDA(h, cudaMemsetAsync(h->d_prof, 0, sizeof(unsigned long long) * (8 + G), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(vt->NT), args, smem, st));
   h->launches = 1;
@@ -563,6 +571,7 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.cooling = p->cooling;
   k.tol = p->tol;
   k.forces_mode = forces_mode;
+  k.attr_only = attr_only ? 1 : 0;
   k.first = first;
   k.count = count;
   k.xy = d_xy;
@@ -731,6 +740,7 @@ extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p
   if (s != BL_OK) return s;
   if (!d_xy) return fail(h, BL_EINVAL, "d_xy is NULL");
   if (((uintptr_t)d_xy) & 7) return fail(h, BL_EINVAL, "d_xy must be 8-byte aligned");
+  if (p->flags & BL_ATTRACTION_ONLY) return fail(h, BL_EINVAL, "BL_ATTRACTION_ONLY is for bl_forces");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   h->last_stream = st;
   h->last_iters = p->iters;

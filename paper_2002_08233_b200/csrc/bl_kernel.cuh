@@ -106,6 +106,7 @@ struct BLKParams {
   int amode, rmode;
   float a_half, r_half;  // (a-1)/2, (r-1)/2: vector coefficients d^(a-1), d^(r-1)
   int forces_mode, first, count;
+  int attr_only;         // forces_mode + BL_ATTRACTION_ONLY: a5 alone (no sweep, R = 0)
   float2 *xy;
   const int *rowptr, *colidx;
   const int *item_ptr, *item_v, *item_k0;
@@ -455,7 +456,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
   const bool tgt_smem = bt <= BL_TGT_CAP;
 
   // (0) stage the batch's targets (frozen coordinates)
-  if (tgt_smem)
+  if (tgt_smem && !p.attr_only)
     for (int i = threadIdx.x; i < bt; i += BL_NT) tgt[i] = __ldcg(p.xy + lo + i);
 
   // (1) attraction items of this batch, spread over all warps of the grid
@@ -493,7 +494,8 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
   __syncthreads();  // targets staged
 
   // (2) repulsion sweep over the CTA's resident sources
-  bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, pf);
+  if (!p.attr_only)
+    bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, pf);
   pf.mark(2);
 }
 
@@ -513,11 +515,13 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
     const int a0 = __ldg(p.item_ptr + v) - ib, a1 = __ldg(p.item_ptr + v + 1) - ib;
     const float2 *row = p.part + (size_t)local * G;
     float rx = 0.f, ry = 0.f;
+    if (!p.attr_only) {
 #pragma unroll 8
-    for (int cc = lane; cc < G; cc += 32) {
-      const float2 q = __ldcg(row + cc);
-      rx += q.x;
-      ry += q.y;
+      for (int cc = lane; cc < G; cc += 32) {
+        const float2 q = __ldcg(row + cc);
+        rx += q.x;
+        ry += q.y;
+      }
     }
     float sx = 0.f, sy = 0.f;
     for (int a = a0 + lane; a < a1; a += 32) {
@@ -1109,6 +1113,23 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
   double step_u = p.step0;
   int prev_owned = 0;
   bool stop = false;
+#ifdef BL_PHASE_TS
+  // warp-time accounting (profiling builds): 0 entry gate, 1 idle (nothing to
+  // grab), 2 dirty wait, 3 units, 4 tile combine, 5 update tasks, 6 control,
+  // 7 total; summed over all warps into p.prof[0..7]
+  unsigned long long wt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long w0 = clock64(), wl = w0;
+#define BL_WT(slot)                      \
+  do {                                   \
+    const long long t_ = clock64();      \
+    wt[slot] += (unsigned long long)(t_ - wl); \
+    wl = t_;                             \
+  } while (0)
+#else
+#define BL_WT(slot) \
+  do {              \
+  } while (0)
+#endif
   for (int ph = 0; ph <= P + 1 && !stop; ++ph) {
     const int s = ph & 1;
     BLPhase f;
@@ -1138,6 +1159,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
           break;
         __nanosleep(32);
       }
+      BL_WT(0);
       if (stop) break;
       __threadfence_block();
     }
@@ -1164,8 +1186,15 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
         stop = true;
         break;
       }
-      if (control()) continue;
-      if (bl_try_update_a(p, f, src4, sh, need)) continue;
+      BL_WT(1);
+      if (control()) {
+        BL_WT(6);
+        continue;
+      }
+      if (bl_try_update_a(p, f, src4, sh, need)) {
+        BL_WT(5);
+        continue;
+      }
       int g = n_all;
       if (vs.a_unit[s] < n_all) {
         if (lane == 0) g = atomicAdd(&sh.a_unit[s], 1);
@@ -1179,15 +1208,25 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
               stop = true;
               break;
             }
-            if (control()) continue;
-            if (bl_try_update_a(p, f, src4, sh, need)) continue;
+            BL_WT(2);
+            if (control()) {
+              BL_WT(6);
+              continue;
+            }
+            if (bl_try_update_a(p, f, src4, sh, need)) {
+              BL_WT(5);
+              continue;
+            }
             if (vs.a_updph >= ph) break;
             __nanosleep(64);
           }
+          BL_WT(2);
           if (stop) break;
           __threadfence_block();
         }
+        BL_WT(1);
         bl_do_unit<T, TP>(p, lo, bt, src4, tgt_s, red_s, part, g, U, geo);
+        BL_WT(3);
         const int tile = g % U.ntt;
         __syncwarp();
         int last = 0;
@@ -1220,6 +1259,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
             bl_token(p, sh, f, need);
           }
           __syncwarp();
+          BL_WT(4);
         }
         continue;
       }
@@ -1239,6 +1279,13 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
     }
     __syncwarp();
   }
+#ifdef BL_PHASE_TS
+  BL_WT(1);
+  wt[7] = (unsigned long long)(clock64() - w0);
+  if (p.prof && lane == 0)
+    for (int k = 0; k < 8; ++k) atomicAdd(p.prof + k, wt[k]);
+#endif
+#undef BL_WT
   __syncthreads();
   if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
 }

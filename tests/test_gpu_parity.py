@@ -540,3 +540,36 @@ def test_driver_selection_C5(env, expect, monkeypatch):
         torch.cuda.synchronize()
         assert bl.bl_driver_name(lay.h) == expect
         assert bl.bl_kernel_name(lay.h) == "bl_layout_kernel<512,8,2>"
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_attraction_only_forces(flags):
+    """BL_ATTRACTION_ONLY (step a5 alone): S_i = attraction + neighbour
+    correction.  Against the oracle: attraction = f(C = 0); the correction =
+    f(default) - f(BL_REPULSE_NEIGHBORS) (the if/else of P:714-719 vs the
+    classic form).  C4, the first 1,500 vertices (hub-heavy rows)."""
+    import paper_2002_08233_b200 as bl
+    g, xy0, cfg = build_config("C4")
+    cnt = 1500
+    got = gpu_forces(g, xy0, 0, cnt, C=cfg.C, K=cfg.K, flags=flags | bl.BL_ATTRACTION_ONLY)
+    fa = oracle.forces(g.n, g.rowptr, g.colidx, xy0, 0, cnt, K=cfg.K, C=0.0)
+    ref = fa.copy()
+    if flags == 0:
+        f_if = oracle.forces(g.n, g.rowptr, g.colidx, xy0, 0, cnt, K=cfg.K, C=cfg.C)
+        f_rn = oracle.forces(g.n, g.rowptr, g.colidx, xy0, 0, cnt, K=cfg.K, C=cfg.C, flags=1)
+        ref = ref + (f_if - f_rn)
+    scale = np.abs(ref).max(1, keepdims=True) + np.abs(fa).max(1, keepdims=True)
+    assert np.all(np.abs(got - ref) <= 2e-4 * scale + 1e-6)
+
+
+def test_attraction_only_rejected_by_layout():
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0 = _small()
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        with pytest.raises(bl.BLError):
+            lay.layout_device(d, iters=1, batch=16, flags=bl.BL_ATTRACTION_ONLY)
+        with pytest.raises(bl.BLError):
+            lay.forces(d, 0, 4, flags=bl.BL_ATTRACTION_ONLY, algo=bl.BL_ALGO_BH)
