@@ -571,7 +571,6 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.cooling = p->cooling;
   k.tol = p->tol;
   k.forces_mode = forces_mode;
-  k.attr_only = attr_only ? 1 : 0;
   k.first = first;
   k.count = count;
   k.xy = d_xy;
