@@ -290,7 +290,8 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
     h->item_ptr[v + 1] = h->item_ptr[v] + (deg + BL_ECH - 1) / BL_ECH;
   }
   h->n_items = h->item_ptr[n];
-  std::vector<int> item_v(std::max(1, h->n_items)), item_k0(std::max(1, h->n_items));
+  // item_k0 has a sentinel: item_k0[n_items] = nnz, so item a ends at item_k0[a + 1]
+  std::vector<int> item_v(std::max(1, h->n_items)), item_k0((size_t)h->n_items + 1, nnz);
   for (int32_t v = 0; v < n; ++v)
     for (int a = h->item_ptr[v]; a < h->item_ptr[v + 1]; ++a) {
       item_v[a] = v;
@@ -479,7 +480,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // the fewer, wider warps of <256,16,6> best; below, <512,8,2> (measured)
   const bool wide = !getenv("BL_NT") && (long long)b * n >= 500000000LL;
   const BLVariant *vt = k.rmode != 0 ? find_variant(512, 8, -1)
-                        : wide       ? find_variant(256, 16, 6)
+                        : wide && !attr_only ? find_variant(256, 16, 6)
                                      : find_variant(h->NT, h->T, h->TP);
   void *kfn = vt->fn;
   // asynchronous phases (bl_run_async) when each half of the partial buffer
