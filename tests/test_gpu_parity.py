@@ -573,3 +573,27 @@ def test_attraction_only_rejected_by_layout():
             lay.layout_device(d, iters=1, batch=16, flags=bl.BL_ATTRACTION_ONLY)
         with pytest.raises(bl.BLError):
             lay.forces(d, 0, 4, flags=bl.BL_ATTRACTION_ONLY, algo=bl.BL_ALGO_BH)
+
+
+@pytest.mark.parametrize("case", _FUZZ)
+def test_fuzz_shapes_async_forced(case, monkeypatch):
+    """The fuzzed shapes with the asynchronous-phase driver forced
+    (BL_ASYNC=1; it takes over wherever the pipelined driver is eligible):
+    one iteration vs the oracle, and a second run bitwise identical."""
+    from blgen import ba_graph
+    monkeypatch.setenv("BL_ASYNC", "1")
+    kind, size, b, K, C, flags = case
+    if kind == "rmat":
+        g = rmat_graph(size, 8, 0.57, 0.19, 0.19, seed=size)
+    elif kind == "ba":
+        g = ba_graph(size, 2, seed=size)
+    else:
+        g = grid_graph(size, size + 3)
+    xy0 = uniform_coords(g.n, 100 + size)
+    p = dict(iters=1, batch=b, K=K, C=C, flags=flags)
+    got, tr, done = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert done == 1
+    assert_positions_close(got, ref, what=f"fuzz async {case}")
+    again, tr2, _ = gpu_layout(g, xy0, **p)
+    assert np.array_equal(got, again) and np.array_equal(tr, tr2)
