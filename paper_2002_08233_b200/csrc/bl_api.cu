@@ -475,7 +475,6 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.red_cap = red_cap_for(k.chunk4);
   k.guided = env_int("BL_GUIDED", 2);
   model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
-  const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   // very large batches (b n >= 5e8 pairs, e.g. 2^20 vertices x 1024) amortise
   // the fewer, wider warps of <256,16,6> best; below, <512,8,2> (measured)
   const bool wide = !getenv("BL_NT") && (long long)b * n >= 500000000LL;
@@ -494,8 +493,19 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
       k.red_cap / 2 / (((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T) >= 2) {
     k.pipelined = 2;
     k.part_nbuf = 3;
+    // fewer, flatter units than the pipelined driver's tail-minimising
+    // quadratic profile: with no phase-end barrier the tail is overlapped, and
+    // each unit's overhead (target loads, partial stores, combine) counts
+    // (measured at C5: 6 sub-ranges, linear profile 0.90 vs 8 quadratic 0.88)
+    k.guided = env_int("BL_GUIDED", 1);
+    k.nsub_max = std::max(2, env_int("BL_NSUB", 6));
     k.afence_gpu = env_int("BL_AFENCE", 0);
+    // only what two phases of nsub_max sub-ranges use: the rest of the shared
+    // memory goes back to L1 (update-task gathers, partial rows)
+    const int tile_slots = ((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T;
+    k.red_cap = std::min(k.red_cap, 2 * k.nsub_max * tile_slots);
   }
+  const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   h->driver_last = forces_mode ? "two-barrier"
                    : k.pipelined == 2 ? "async"

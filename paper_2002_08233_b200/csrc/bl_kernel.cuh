@@ -59,11 +59,12 @@
 struct BLUnits {
   int ntt, nc, nsub;
 };
-__host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty, int red_cap) {
+__host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty, int red_cap,
+                                            int nsub_max = BL_NSUB_MAX) {
   BLUnits u;
   u.ntt = (bt + 32 * T - 1) / (32 * T);
   int cap = red_cap / (u.ntt * 32 * T);
-  if (cap > BL_NSUB_MAX) cap = BL_NSUB_MAX;
+  if (cap > nsub_max) cap = nsub_max;
   int nc = clean4 / BL_MIN_UNIT4;
   if (nc > cap - (dirty ? 1 : 0)) nc = cap - (dirty ? 1 : 0);
   u.nc = nc < 1 ? 1 : nc;
@@ -74,11 +75,13 @@ __host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirt
 // start (in the concatenated clean domain of length L) of clean sub-range k
 // of nc.  Sizes decrease so that the units grabbed last (the tail of a
 // batch, when warps run out of work) are small:
+//   profile 0: equal sizes
 //   profile 1: weights nc, nc-1, ..., 1        (linear)
 //   profile 2: weights nc^2, (nc-1)^2, ..., 1  (quadratic; the default)
 __device__ __forceinline__ long long bl_sq_sum(long long m) { return m * (m + 1) * (2 * m + 1) / 6; }
 __device__ __forceinline__ int bl_guided_start(int k, int nc, int L, int profile) {
   long long W, cum;
+  if (profile == 0) return (int)(((long long)L * k) / nc);  // uniform
   if (profile == 2) {
     W = bl_sq_sum(nc);
     cum = W - bl_sq_sum(nc - k);
@@ -101,6 +104,7 @@ struct BLKParams {
   int chunk4;            // float4 slots (2 sources each) per CTA chunk
   int red_cap;           // float2 slots of the shared partial buffer
   int guided;            // sub-range size profile (bl_guided_start)
+  int nsub_max;          // async driver: sub-ranges per target tile (incl. the dirty one)
   // (a, r)-energy model (reading C15): attraction d^a/K, repulsion C K^2 d^r;
   // amode 0..3: a = 2, 1, 0, 3 (no pow), 4: general; rmode 0: r = -1, 1: general
   int amode, rmode;
@@ -1192,7 +1196,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
     const int bt = has_R ? min(p.b, p.n - lo) : 0;
     const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
     BLUnits U = {1, 0, 0};
-    if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, half);
+    if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, half, p.nsub_max);
     const int n_all = has_R ? U.ntt * U.nsub : 0;
     const int n_clean = has_R ? U.ntt * U.nc : 0;
     const int need = (has_R ? U.ntt : 0) + (ph > 0 ? 1 : 0) + f.owned;
@@ -1304,8 +1308,10 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
 #ifdef BL_PHASE_TS
   BL_WT(1);
   wt[7] = (unsigned long long)(clock64() - w0);
-  if (p.prof && lane == 0)
+  if (p.prof && lane == 0) {
     for (int k = 0; k < 8; ++k) atomicAdd(p.prof + k, wt[k]);
+    atomicAdd(p.prof + 8 + c, wt[3] + wt[4] + wt[5] + wt[6]);  // this CTA's busy warp time
+  }
 #endif
 #undef BL_WT
   __syncthreads();

@@ -37,4 +37,10 @@ with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
     out = {"config": a.config, "iters": a.iters, "driver": bl.bl_driver_name(lay.h),
            "kernel": bl.bl_kernel_name(lay.h), "ms": st.elapsed_time(en),
            "warp_time_fraction": {n: pr[i] / tot for i, n in enumerate(names)}}
+    busy = pr[8:8 + torch.cuda.get_device_properties(0).multi_processor_count]
+    busy = busy / busy.mean()
+    out["cta_busy_rel"] = {"min": float(busy.min()), "max": float(busy.max()),
+                           "std": float(busy.std()),
+                           "slowest_ctas": [int(i) for i in busy.argsort()[-8:][::-1]],
+                           "fastest_ctas": [int(i) for i in busy.argsort()[:8]]}
     print(json.dumps(out, indent=1))
