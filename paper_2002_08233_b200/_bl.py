@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libbl.so")
+# BL_LIBRARY: another build of the same ABI (same-box A/B measurements only)
+_SO = os.environ.get("BL_LIBRARY") or os.path.join(_HERE, "libbl.so")
 
 BL_OK, BL_EINVAL, BL_ENOMEM, BL_ECUDA, BL_ESTATE = 0, -1, -2, -3, -4
 BL_REPULSE_NEIGHBORS = 1

@@ -741,16 +741,48 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       }
       return;
     }
+    // long rows: a lane's next 8 entries are loaded before any is used (two
+    // dependent L2 round trips per 256 entries; per-lane order unchanged).
+    // Measured: +1.4 % at C5 (async driver: shorter updates, less waiting on
+    // other CTAs), -1..2 % on the latency-bound configs, which keep the
+    // unrolled loop below.
+    if (p.pipelined != 2) {
 #pragma unroll 4
-    for (int k = k0 + lane; k < k1; k += 32) {
-      const int j = __ldg(p.colidx + k);
-      const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
-      const float dx = cj.x - ci.x, dy = cj.y - ci.y;
-      const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
-      const float rs = bl_rsqrt(d2);
-      const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
-      sx = fmaf(coef, dx, sx);
-      sy = fmaf(coef, dy, sy);
+      for (int k = k0 + lane; k < k1; k += 32) {
+        const int j = __ldg(p.colidx + k);
+        const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        const float dx = cj.x - ci.x, dy = cj.y - ci.y;
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+        const float rs = bl_rsqrt(d2);
+        const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+        sx = fmaf(coef, dx, sx);
+        sy = fmaf(coef, dy, sy);
+      }
+      return;
+    }
+    for (int base = k0; base < k1; base += 256) {
+      int jj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = base + lane + 32 * u;
+        jj[u] = k < k1 ? __ldg(p.colidx + k) : -1;
+      }
+      float2 cj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jj[u];
+        cj[u] = j < 0 ? ci : (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (jj[u] < 0) continue;
+        const float dx = cj[u].x - ci.x, dy = cj[u].y - ci.y;
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+        const float rs = bl_rsqrt(d2);
+        const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+        sx = fmaf(coef, dx, sx);
+        sy = fmaf(coef, dy, sy);
+      }
     }
   };
   if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});  // branch hoisted out of the loop
