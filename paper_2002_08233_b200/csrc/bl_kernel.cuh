@@ -1105,10 +1105,12 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
 //     of ph+1 staged), the update tasks of phase ph done (their sources are
 //     clean in ph+1), and slot (ph+1)&1 released by every warp of phase ph-1
 //     (the last warp to leave a phase resets its slot).
-// At most two phases are live in a CTA.  part has three buffers: the tile
-// combines of phase ph can run before barrier ph-1 completes, while other
-// CTAs' update tasks of phase ph-2 still read part[(ph-3) % 3]... never the
-// same buffer.  Results are independent of which warp ran which task (fixed
+// At most two phases are live in a CTA.  part has three buffers: a CTA
+// enters phase ph once barrier ph-2 has completed, so its tile combines of
+// phase ph (into part[ph % 3]) can run while slower CTAs' update tasks of
+// phase ph-1 still read the partials of batch ph-2 (part[(ph-2) % 3]) and
+// after barrier ph-1 everyone reads part[(ph-1) % 3]: three distinct
+// buffers.  Results are independent of which warp ran which task (fixed
 // summation orders), as in the pipelined driver.
 __device__ __forceinline__ bool bl_try_update_a(const BLKParams &p, const BLPhase &f,
                                                 float4 *src4, BLShared &sh, int need) {
