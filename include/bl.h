@@ -148,8 +148,12 @@ bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int32_t count, 
 
 /* BL_ALGO_BH: number of quadtree nodes the last bl_layout_device /
  * bl_layout / bl_forces call visited in Alg. S2 traversals (summed over all
- * queries; leaves and accepted or opened cells each count once).  Synchronises
- * h's last stream.  *visits = 0 after an exact-algorithm call. */
+ * queries; leaves and accepted or opened cells each count once).  Layout
+ * calls walk the tree for every vertex at the start of each iteration (the
+ * walk depends only on the iteration-start tree and the vertex's own,
+ * not yet moved, position -- reading B5), so an iteration stopped early by
+ * max_batches still counts all n walks.  Synchronises h's last stream.
+ * *visits = 0 after an exact-algorithm call. */
 bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits);
 
 /* ---- layout quality metrics, §3.7; readings M1-M4 in DESIGN.md §3.

@@ -82,6 +82,8 @@ struct bl_ctx {
   bool last_bh = false;
   float2 *d_attr_bh = nullptr;
   unsigned *d_aflag = nullptr;
+  float2 *d_cellf = nullptr;  // BH per-iteration precomputation
+  int *d_nleaf = nullptr, *d_leafv = nullptr;
   // quality-metric scratch (allocated per call)
 };
 
@@ -366,6 +368,9 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_visits);
   cudaFree(h->d_attr_bh);
   cudaFree(h->d_aflag);
+  cudaFree(h->d_cellf);
+  cudaFree(h->d_nleaf);
+  cudaFree(h->d_leafv);
   delete h;
 }
 
@@ -558,6 +563,9 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
     ALLOC(h->d_visits, G);
     ALLOC(h->d_attr_bh, std::max(1, h->n_items));
     ALLOC(h->d_aflag, std::max(1, h->n_items));
+    ALLOC(h->d_cellf, n);
+    ALLOC(h->d_nleaf, n);
+    ALLOC(h->d_leafv, (size_t)n * BH_LCAP);
 #undef ALLOC
     h->bh_ready = true;
   }
@@ -609,6 +617,10 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.item_k0 = h->d_item_k0;
   k.attr = h->d_attr_bh;
   k.aflag = h->d_aflag;
+  k.cellf = h->d_cellf;
+  k.nleaf = h->d_nleaf;
+  k.leafv = h->d_leafv;
+  k.precompute = !forces_mode && env_int("BL_BH_PRE", 1) != 0;
   k.e_cta = h->d_e_cta;
   k.energy = h->d_energy;
   k.iters_done = h->d_iters_done;

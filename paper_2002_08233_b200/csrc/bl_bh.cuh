@@ -37,6 +37,7 @@
 #define BH_FCAP 512  // frontier entries per buffer per warp
 #define BH_TOP_LEVEL 4  // tree levels 0..4 are copied to shared memory per CTA
 #define BH_TOP_MAX 352  // >= 1 + 4 + 16 + 64 + 256
+#define BH_LCAP 32      // leaf vertices recorded per query (one per lane)
 
 struct BHKParams {
   int n, b, nb, iters, max_batches;
@@ -67,6 +68,17 @@ struct BHKParams {
   float2 *f_out;
   unsigned long long *visits;  // [G] node visits per CTA (for the roofline)
   float2 *pend;                // [2][b] new coordinates of the last two batches
+  // per-iteration precomputation (layout mode): the MAC decisions and the
+  // accepted cells' terms depend only on the iteration-start tree and the
+  // query's own position, which does not move before its batch (reading B5),
+  // so each vertex's cell sum and its list of leaf vertices are computed once
+  // per iteration for all n vertices at once; a batch then adds the leaf
+  // terms at the live coordinates.  nleaf < 0: list overflow, the batch
+  // traverses the tree for that vertex as before.
+  float2 *cellf;               // [n]
+  int *nleaf;                  // [n]
+  int *leafv;                  // [n][BH_LCAP]
+  int precompute;              // 1: use the above
   // attraction of high-degree ("split") vertices, edge-parallel: rows cut in
   // items of <= BL_ECH entries (the context's item lists), one partial per
   // item, published with a release flag stamped with the batch number
@@ -771,6 +783,80 @@ __device__ __forceinline__ float2 bh_force_warp(const BHKParams &p, BHShared &sh
   return make_float2(fx + fa.x, fy + fa.y);
 }
 
+// Per-iteration precomputation for all n queries (one per thread, queries in
+// Morton order so a warp's lanes walk similar paths): the full Alg. S2 walk
+// with the skip pointers from the root; accepted cells accumulate into
+// cellf[v] (fixed per iteration, reading B5), leaf vertices are recorded
+// (at most BH_LCAP; more -> nleaf = -1 and the batch traverses for v).
+// Node visits are counted here for every recorded query.
+__device__ __forceinline__ void bh_precompute(const BHKParams &p, unsigned long long &vis) {
+  const int G = gridDim.x, c = blockIdx.x;
+  const int Nn = __ldcg(p.nnodes);
+  for (int s = c * blockDim.x + threadIdx.x; s < p.n; s += G * blockDim.x) {
+    const int v = __ldcg(p.valA + s);
+    const float2 q = __ldcg(p.xy + v);
+    float fx = 0.f, fy = 0.f;
+    int nl = 0;
+    unsigned long long vv = 0;
+    int *lst = p.leafv + (size_t)v * BH_LCAP;
+    int t = 0;
+    while (t < Nn) {
+      const BHNode nd = bh_load(p, t);
+      ++vv;
+      if (nd.B.x & (1 << 16)) {
+        const int cnt = nd.B.z;
+        for (int k = 0; k < cnt; ++k) {
+          const int j = cnt == 1 ? nd.C.w : __ldcg(p.valA + nd.B.y + k);
+          if (j == v) continue;
+          if (nl < BH_LCAP) lst[nl] = j;
+          ++nl;
+        }
+        t = nd.B.w;
+      } else if (bh_mac(p, nd.A, q.x, q.y, fx, fy)) {
+        t = nd.B.w;
+      } else {
+        t = t + 1;
+      }
+    }
+    const bool ok = nl <= BH_LCAP;
+    p.cellf[v] = make_float2(fx, fy);
+    p.nleaf[v] = ok ? nl : -1;
+    if (ok) vis += vv;
+  }
+}
+
+// Force of vertex v (one warp) from its precomputed cell sum and leaf list:
+// the leaf terms at the live coordinates (one leaf vertex per lane) +
+// attraction.  Returns the warp-summed force on every lane.
+__device__ __forceinline__ float2 bh_force_pre(const BHKParams &p, int v, float2 cv, int nl,
+                                               int plo, int phi, const float2 *pend,
+                                               unsigned stamp) {
+  const int lane = threadIdx.x & 31;
+  const bool split = __ldg(p.item_ptr + v + 1) - __ldg(p.item_ptr + v) > 1;
+  float fx = 0.f, fy = 0.f;
+  if (lane < nl) {
+    const int j = __ldcg(p.leafv + (size_t)v * BH_LCAP + lane);
+    const float2 cj = bh_live(p, j, plo, phi, pend);
+    const float dx = cj.x - cv.x, dy = cj.y - cv.y;
+    const float d2 = fmaf(dx, dx, dy * dy);
+    if (d2 > 0.f) {
+      const float r = bh_rep_weight(p, d2);
+      fx = fmaf(-r, dx, fx);
+      fy = fmaf(-r, dy, fy);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+  }
+  const float2 cf = __ldcg(p.cellf + v);
+  const float2 fa = split ? bh_attr_gather(p, v, stamp)
+                          : bh_attr_range(p, __ldg(p.rowptr + v), __ldg(p.rowptr + v + 1), cv,
+                                          plo, phi, pend);
+  return make_float2(fx + cf.x + fa.x, fy + cf.y + fa.y);
+}
+
 // Fixed-order sum of the G per-CTA fp64 energies by one warp (identical in
 // every CTA, so the tol decision is too).
 __device__ __forceinline__ double bh_energy_sum(const BHKParams &p) {
@@ -808,6 +894,10 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
     }
     pf.mark(4);
     bh_build_tree<NT>(p, sh, bar_target, unit_dummy_ptr, pf);  // Alg. S3 lines 5-8
+    if (p.precompute) {
+      bh_precompute(p, vis);
+      bl_grid_sync(p.bar, bar_target, unit_dummy_ptr);
+    }
     double e_acc = 0.0;
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b, bt = min(p.b, p.n - lo);
@@ -826,7 +916,9 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
       for (int i = warp * G + c; i < bt; i += GW) {
         const int v = lo + i;
         const float2 cv = __ldcg(p.xy + v);
-        const float2 f = bh_force_warp(p, sh, v, cv, plo, phi, pend_prev, stamp, vis);
+        const int nl = p.precompute ? __ldcg(p.nleaf + v) : -1;
+        const float2 f = nl >= 0 ? bh_force_pre(p, v, cv, nl, plo, phi, pend_prev, stamp)
+                                 : bh_force_warp(p, sh, v, cv, plo, phi, pend_prev, stamp, vis);
         if (lane == 0) {
           const double q = (double)f.x * f.x + (double)f.y * f.y;
           float2 nv = cv;

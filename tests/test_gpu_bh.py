@@ -195,3 +195,48 @@ def test_C6_million_vertices_shadowed():
     got, visits = gpu_forces(g, xy0, 0, b, with_visits=True, **_bh())
     _, ref_visits = oracle.bh_forces(g.n, g.rowptr, g.colidx, xy0, xy0, 0, b)
     assert visits == ref_visits
+
+
+@pytest.mark.parametrize("name,theta", [("C3b256", 1.2), ("C4", 1.2), ("C4", 0.5)])
+def test_layout_visits_one_iteration(name, theta):
+    """Layout mode precomputes every vertex's walk at the iteration start
+    (accepted cells fixed per iteration, leaves later at live coordinates,
+    reading B5); vertices whose leaf list overflows walk the tree in their
+    batch.  Either way each vertex's Alg. S2 walk of iteration 0 is the
+    oracle's: the node-visit totals match exactly, and the positions after
+    the iteration's first batch too."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0, cfg = build_config(name)
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=1, batch=cfg.batch, **_bh(theta=theta))
+        torch.cuda.synchronize()
+        visits = bl.bl_last_visits(lay.h)
+    _, _, _, ref_visits = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=1,
+                                           batch=cfg.batch, theta=theta)
+    assert visits == ref_visits
+    got, _, _ = gpu_layout(g, xy0, iters=1, batch=cfg.batch, max_batches=1, **_bh(theta=theta))
+    ref, _, _, _ = oracle.bh_layout(g.n, g.rowptr, g.colidx, xy0, iters=1, batch=cfg.batch,
+                                    max_batches=1, theta=theta)
+    assert_positions_close(got, ref, what=f"BH {name} theta {theta} one batch")
+
+
+def test_precompute_off_matches(monkeypatch):
+    """BL_BH_PRE=0 (every vertex walks the tree in its batch) and the default
+    precomputation agree on one batch to the tolerance (summation order
+    differs) and on the iteration's visit total exactly."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0, cfg = build_config("C4")
+    out = {}
+    for pre in ("1", "0"):
+        monkeypatch.setenv("BL_BH_PRE", pre)
+        with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+            d = torch.from_numpy(xy0.copy()).cuda()
+            lay.layout_device(d, iters=1, batch=cfg.batch, max_batches=1, **_bh())
+            torch.cuda.synchronize()
+            out[pre] = d.cpu().numpy()
+    assert_positions_close(out["1"], out["0"].astype(np.float64), what="precompute on/off")
