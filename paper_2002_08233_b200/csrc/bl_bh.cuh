@@ -645,10 +645,10 @@ __device__ __forceinline__ void bh_walk_subtree(const BHKParams &p, int k, int e
 // Attraction sum over CSR entries [k0, k1) of vertex v at cv (one warp,
 // lanes strided, fixed butterfly): f_a = d^2/K along the unit vector
 // (Alg. S3 lines 15-17), live neighbour coordinates.
-__device__ __forceinline__ float2 bh_attr_range(const BHKParams &p, int k0, int k1, float2 cv,
-                                                int plo, int phi, const float2 *pend) {
+__device__ __forceinline__ void bh_attr_lane(const BHKParams &p, int k0, int k1, float2 cv,
+                                             int plo, int phi, const float2 *pend, float &fx,
+                                             float &fy) {
   const int lane = threadIdx.x & 31;
-  float fx = 0.f, fy = 0.f;
   for (int k = k0 + lane; k < k1; k += 32) {
     const float2 cj = bh_live(p, __ldg(p.colidx + k), plo, phi, pend);
     const float dx = cj.x - cv.x, dy = cj.y - cv.y;
@@ -666,6 +666,11 @@ __device__ __forceinline__ float2 bh_attr_range(const BHKParams &p, int k0, int 
       fy = fmaf(at * p.invK, dy, fy);
     }
   }
+}
+__device__ __forceinline__ float2 bh_attr_range(const BHKParams &p, int k0, int k1, float2 cv,
+                                                int plo, int phi, const float2 *pend) {
+  float fx = 0.f, fy = 0.f;
+  bh_attr_lane(p, k0, k1, cv, plo, phi, pend, fx, fy);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     fx += __shfl_xor_sync(0xffffffffu, fx, o);
@@ -832,11 +837,18 @@ __device__ __forceinline__ float2 bh_force_pre(const BHKParams &p, int v, float2
                                                int plo, int phi, const float2 *pend,
                                                unsigned stamp) {
   const int lane = threadIdx.x & 31;
-  const bool split = __ldg(p.item_ptr + v + 1) - __ldg(p.item_ptr + v) > 1;
-  float fx = 0.f, fy = 0.f;
-  if (lane < nl) {
-    const int j = __ldcg(p.leafv + (size_t)v * BH_LCAP + lane);
-    const float2 cj = bh_live(p, j, plo, phi, pend);
+  // first-level loads of both chains together: the leaf id and the row bounds
+  const int j = lane < nl ? __ldcg(p.leafv + (size_t)v * BH_LCAP + lane) : -1;
+  const int ip0 = __ldg(p.item_ptr + v), ip1 = __ldg(p.item_ptr + v + 1);
+  const int k0 = __ldg(p.rowptr + v), k1 = __ldg(p.rowptr + v + 1);
+  const float2 cf = __ldcg(p.cellf + v);
+  const bool split = ip1 - ip0 > 1;
+  // per-lane sums of both chains, one reduction at the end
+  float fx = 0.f, fy = 0.f, ax = 0.f, ay = 0.f;
+  float2 cj = cv;
+  if (j >= 0) cj = bh_live(p, j, plo, phi, pend);
+  if (!split) bh_attr_lane(p, k0, k1, cv, plo, phi, pend, ax, ay);
+  if (j >= 0) {
     const float dx = cj.x - cv.x, dy = cj.y - cv.y;
     const float d2 = fmaf(dx, dx, dy * dy);
     if (d2 > 0.f) {
@@ -849,12 +861,15 @@ __device__ __forceinline__ float2 bh_force_pre(const BHKParams &p, int v, float2
   for (int o = 16; o > 0; o >>= 1) {
     fx += __shfl_xor_sync(0xffffffffu, fx, o);
     fy += __shfl_xor_sync(0xffffffffu, fy, o);
+    ax += __shfl_xor_sync(0xffffffffu, ax, o);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o);
   }
-  const float2 cf = __ldcg(p.cellf + v);
-  const float2 fa = split ? bh_attr_gather(p, v, stamp)
-                          : bh_attr_range(p, __ldg(p.rowptr + v), __ldg(p.rowptr + v + 1), cv,
-                                          plo, phi, pend);
-  return make_float2(fx + cf.x + fa.x, fy + cf.y + fa.y);
+  if (split) {
+    const float2 g = bh_attr_gather(p, v, stamp);
+    ax = g.x;
+    ay = g.y;
+  }
+  return make_float2(fx + cf.x + ax, fy + cf.y + ay);
 }
 
 // Fixed-order sum of the G per-CTA fp64 energies by one warp (identical in
@@ -897,6 +912,7 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
     if (p.precompute) {
       bh_precompute(p, vis);
       bl_grid_sync(p.bar, bar_target, unit_dummy_ptr);
+      pf.mark(7);
     }
     double e_acc = 0.0;
     for (int t = 0; t < p.nb; ++t) {

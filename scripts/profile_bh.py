@@ -40,7 +40,7 @@ with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
     pr = bl.bl_debug_profile(lay.h).astype(np.float64) / mhz
-    names = ["bbox", "sort", "nodes", "centroids", "iter_glue", "forces", "barrier", "unused"]
+    names = ["bbox", "sort", "nodes", "centroids", "iter_glue", "forces", "barrier", "precompute"]
     nb = -(-g.n // cfg.batch)
     out = {"config": a.config, "theta": a.theta, "noedges": a.noedges, "iters": a.iters, "wall_ms": dt * 1e3,
            "us_per_iter": {k: round(v / a.iters, 1) for k, v in zip(names, pr[:8])},
