@@ -200,7 +200,7 @@ const char *bl_kernel_name(const bl_ctx *h);
 
 /* How the last layout call on h sequenced its dependent batches (DESIGN.md
  * §4): "async" (one grid barrier per batch, no CTA-wide barrier between
- * phases; b n >= 2^25), "pipelined" (one grid barrier per batch), "two-barrier"
+ * phases; b n >= 2^22), "pipelined" (one grid barrier per batch), "two-barrier"
  * (phase R; barrier; phase U; barrier), "cluster" (single thread-block cluster)
  * or "bh" (BatchLayoutBH); "" before any call.  Static storage owned by h. */
 const char *bl_driver_name(const bl_ctx *h);

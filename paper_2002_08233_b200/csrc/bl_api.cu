@@ -489,11 +489,12 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   void *kfn = vt->fn;
   // asynchronous phases (bl_run_async) when each half of the partial buffer
   // still holds >= 2 sub-ranges of the batch's target tiles, and the batch's
-  // pair work is large (measured: C5, b n = 2.7e8, +13 %; C4, 8.4e6, +0.7 %;
-  // C2 / C3 b=256, ~2e6, -20 %: latency-bound batches keep the pipelined
+  // pair work is not tiny (measured with the tuned driver, same box: C5,
+  // b n = 2.7e8, +13 %; C3 b=1024, 1.1e7, +10 %; C4, 8.4e6, +2 %; C3 b=256,
+  // 2.8e6, -16 %; C2, 1.5e6, -22 %: latency-bound batches keep the pipelined
   // driver).  BL_ASYNC=1 / 0 forces it on / off.
   const int async_env = env_int("BL_ASYNC", -1);
-  const bool async_auto = (long long)b * n >= (1LL << 25);
+  const bool async_auto = (long long)b * n >= (1LL << 22);
   if (k.pipelined && (async_env == 1 || (async_env < 0 && async_auto)) &&
       k.red_cap / 2 / (((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T) >= 2) {
     k.pipelined = 2;

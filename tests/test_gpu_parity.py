@@ -527,7 +527,7 @@ def test_async_driver_bitwise_repeatable(name, monkeypatch):
 @pytest.mark.parametrize("env,expect", [({}, "async"), ({"BL_ASYNC": "0"}, "pipelined"),
                                         ({"BL_PIPELINE": "0"}, "two-barrier")])
 def test_driver_selection_C5(env, expect, monkeypatch):
-    """C5 (b n = 2.7e8 >= 2^25) runs the asynchronous-phase driver by default;
+    """C5 (b n = 2.7e8 >= 2^22) runs the asynchronous-phase driver by default;
     bl_driver_name reports what ran (one batch)."""
     import torch
 
@@ -597,3 +597,20 @@ def test_fuzz_shapes_async_forced(case, monkeypatch):
     assert_positions_close(got, ref, what=f"fuzz async {case}")
     again, tr2, _ = gpu_layout(g, xy0, **p)
     assert np.array_equal(got, again) and np.array_equal(tr, tr2)
+
+
+@pytest.mark.parametrize("name,expect", [("C2", "pipelined"), ("C3b256", "pipelined"),
+                                         ("C3b1024", "async"), ("C4", "async"),
+                                         ("C1", "cluster"), ("C3b64", "cluster")])
+def test_default_driver_per_config(name, expect):
+    """The measured crossovers: single cluster for b n <= 1e6, pipelined
+    below b n = 2^22, asynchronous phases above."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0, cfg = build_config(name)
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=1, batch=cfg.batch, max_batches=2)
+        torch.cuda.synchronize()
+        assert bl.bl_driver_name(lay.h) == expect
