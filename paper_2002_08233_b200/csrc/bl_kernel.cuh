@@ -59,6 +59,8 @@
 struct BLUnits {
   int ntt, nc, nsub;
 };
+// Precondition with a dirty range: red_cap holds >= 2 sub-ranges of every
+// tile (the host's driver eligibility checks; tests/cpp/test_units.cu).
 __host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty, int red_cap,
                                             int nsub_max = BL_NSUB_MAX) {
   BLUnits u;
@@ -78,8 +80,8 @@ __host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirt
 //   profile 0: equal sizes
 //   profile 1: weights nc, nc-1, ..., 1        (linear)
 //   profile 2: weights nc^2, (nc-1)^2, ..., 1  (quadratic; the default)
-__device__ __forceinline__ long long bl_sq_sum(long long m) { return m * (m + 1) * (2 * m + 1) / 6; }
-__device__ __forceinline__ int bl_guided_start(int k, int nc, int L, int profile) {
+__host__ __device__ inline long long bl_sq_sum(long long m) { return m * (m + 1) * (2 * m + 1) / 6; }
+__host__ __device__ inline int bl_guided_start(int k, int nc, int L, int profile) {
   long long W, cum;
   if (profile == 0) return (int)(((long long)L * k) / nc);  // uniform
   if (profile == 2) {
@@ -341,7 +343,7 @@ __device__ __forceinline__ void bl_sweep_range(const float4 *src4, int s0, int s
 struct BLGeom {
   int full4, last4, d_lo, d_hi, clean4;
 };
-__device__ __forceinline__ BLGeom bl_geom(int c, int G, int n, int k_lo, int owned) {
+__host__ __device__ inline BLGeom bl_geom(int c, int G, int n, int k_lo, int owned) {
   BLGeom g;
   const int m_c = c < n ? (n - 1 - c) / G + 1 : 0;
   g.full4 = m_c >> 1;
