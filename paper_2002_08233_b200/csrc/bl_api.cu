@@ -505,6 +505,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     // (measured at C5: 6 sub-ranges, linear profile 0.90 vs 8 quadratic 0.88)
     k.guided = env_int("BL_GUIDED", 1);
     k.nsub_max = std::max(2, env_int("BL_NSUB", 6));
+    k.spin_max = (unsigned)std::max(32, env_int("BL_SPIN", 512));
     k.afence_gpu = env_int("BL_AFENCE", 0);
     // only what two phases of nsub_max sub-ranges use: the rest of the shared
     // memory goes back to L1 (update-task gathers, partial rows)

@@ -107,6 +107,7 @@ struct BLKParams {
   int red_cap;           // float2 slots of the shared partial buffer
   int guided;            // sub-range size profile (bl_guided_start)
   int nsub_max;          // async driver: sub-ranges per target tile (incl. the dirty one)
+  unsigned spin_max;     // async driver: longest back-off sleep of a waiting warp (ns)
   // (a, r)-energy model (reading C15): attraction d^a/K, repulsion C K^2 d^r;
   // amode 0..3: a = 2, 1, 0, 3 (no pow), 4: general; rmode 0: r = -1, 1: general
   int amode, rmode;
@@ -1175,6 +1176,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
   double step_u = p.step0;
   int prev_owned = 0;
   bool stop = false;
+  unsigned gate_ns = 32, idle_ns = 32;  // spin back-off (ns), capped at p.spin_max
 #ifdef BL_PHASE_TS
   // warp-time accounting (profiling builds): 0 entry gate, 1 idle (nothing to
   // grab), 2 dirty wait, 3 units, 4 tile combine, 5 update tasks, 6 control,
@@ -1219,8 +1221,10 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
         if (vs.a_gen[s] == ph && (ph == 1 || vs.ready >= ph - 1) &&
             (prev_owned == 0 || vs.a_updph >= ph - 1))
           break;
-        __nanosleep(32);
+        __nanosleep(gate_ns);
+        gate_ns = min(2 * gate_ns, p.spin_max);
       }
+      gate_ns = 32;
       BL_WT(0);
       if (stop) break;
       __threadfence_block();
@@ -1251,10 +1255,12 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
       BL_WT(1);
       if (control()) {
         BL_WT(6);
+        idle_ns = 32;
         continue;
       }
       if (bl_try_update_a(p, f, src4, sh, need)) {
         BL_WT(5);
+        idle_ns = 32;
         continue;
       }
       int g = n_all;
@@ -1263,6 +1269,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
         g = __shfl_sync(0xffffffffu, g, 0);
       }
       if (g < n_all) {
+        idle_ns = 32;
         if (g >= n_clean) {
           // dirty sub-range: needs this CTA's updates of batch q1; help until done
           for (;;) {
@@ -1325,10 +1332,14 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
         }
         continue;
       }
-      // nothing left to grab: leave once control is claimed and every update taken
+      // nothing left to grab: leave once control is claimed and every update
+      // taken; back off exponentially (spinning warps issue integer work on
+      // the FMA pipe that the sweeping warps need)
       if ((ph == 0 || vs.ctrl_claim >= ph) && vs.a_unext[s] >= f.owned) break;
-      __nanosleep(32);
+      __nanosleep(idle_ns);
+      idle_ns = min(2 * idle_ns, p.spin_max);
     }
+    idle_ns = 32;
     if (stop) break;
     // leave the phase; the last warp out releases slot s for phase ph+2
     if (lane == 0 && atomicAdd(&sh.a_exit[s], 1) == BL_NW - 1) {
