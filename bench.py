@@ -72,6 +72,20 @@ def load_traffic(workload: str, kernel: str):
     return float(e["bytes_per_launch"]), e.get("source")
 
 
+def load_pipes(workload: str, kernel: str):
+    """Pipe utilisation of the timed kernel from the committed ncu capture
+    (profiles/pipes.json: XU = MUFU, FMA, issue-active, % of peak sustained),
+    or None."""
+    p = os.path.join(ROOT, "profiles", "pipes.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        e = json.load(fh).get(workload)
+    if not e or e.get("kernel") != kernel:
+        return None
+    return e
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -144,12 +158,18 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def workload_desc(name, g, cfg):
+def workload_desc(name, g, cfg, args=None, world=1):
+    """The `config` object of the JSON line -- identical for both arms."""
+    a = getattr(args, "a", 2.0) if args is not None else 2.0
+    r = getattr(args, "r", -1.0) if args is not None else -1.0
     return {
         "workload": f"{name}: {cfg.desc}, batch {cfg.batch}, {cfg.iters} iterations, exact all-pairs "
                     "repulsion, fp32 coords U[0,1)^2 seed 42",
         "n": g.n, "nnz": int(g.nnz), "batch": cfg.batch, "iters": cfg.iters,
         "K": cfg.K, "C": cfg.C, "step0": cfg.step0, "cooling": cfg.cooling,
+        "energy_model": {"a": a, "r": r},
+        "l2": "flushed (512 MiB write) before every timed step (GPU arm)",
+        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
     }
 
 
@@ -219,7 +239,7 @@ def bench_reference(args, name, g, xy0, cfg, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_desc(name, g, cfg),
+        "data": "synthetic", "config": workload_desc(name, g, cfg, args, world),
         "iters_per_sec": value / (g.n * (g.n - 1.0)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": sample},
@@ -267,10 +287,14 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
     barrier(world)
     ms = [a.elapsed_time(b) for a, b in ev]
-    t_local = sum(ms) / 1e3
-    t_max = max_over_ranks(t_local, world, dev if world > 1 and args.backend == "nccl" else None)
+    # per-step device time: the MEDIAN of the K timed steps,
+    # max over ranks; the mean is reported beside it
+    t_step = float(np.median(ms)) / 1e3
+    t_max = max_over_ranks(t_step, world, dev if world > 1 and args.backend == "nccl" else None)
+    t_mean = max_over_ranks(sum(ms) / 1e3 / args.steps, world,
+                            dev if world > 1 and args.backend == "nccl" else None)
     pairs_per_step = cfg.iters * g.n * (g.n - 1.0)
-    value = aggregate_value(args.steps * pairs_per_step, world, t_max)
+    value = aggregate_value(pairs_per_step, world, t_max)
     e_last, trace, done = lay.energy(trace_len=cfg.iters)
     assert done == cfg.iters
 
@@ -295,18 +319,21 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     sm_max = float(clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     mufu_per_pair = 1 if args.r == -1.0 else 2   # r != -1: lg2 + ex2
-    peak = nsm * MUFU_PER_CLK_SM * sm_max * 1e6 / mufu_per_pair
-    achieved = pairs_per_step / (t_local / args.steps)
+    # SFU rate per SM per clock measured on this box (bl_microbench: MUFU.RCP
+    # with clock64 on every SM), rounded to the lane count it resolves
+    mb_rates = [float(x) for x in bl.bl_microbench()]
+    mufu_clk = float(round(mb_rates[1])) if 8 <= mb_rates[1] <= 32 else float(MUFU_PER_CLK_SM)
+    peak = nsm * mufu_clk * sm_max * 1e6 / mufu_per_pair
+    achieved = pairs_per_step / t_step
     kname = bl.bl_kernel_name(lay.h)
     traffic, traffic_src = load_traffic(name, kname)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_max, "ms_per_step_mean": 1e3 * t_mean,
+        "ms_per_step_all": [round(x, 4) for x in ms], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": dict(workload_desc(name, g, cfg), energy_model={"a": args.a, "r": args.r},
-                       l2="flushed (512 MiB write) before every timed step",
-                       parallelism=f"replicas x{world}" if world > 1 else "1 GPU"),
-        "iters_per_sec": world * args.steps * cfg.iters / t_max,
+        "config": workload_desc(name, g, cfg, args, world),
+        "iters_per_sec": world * cfg.iters / t_max,
         "roofline": {
             "bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT,
             "frac": achieved / peak, "traffic": traffic,
@@ -314,11 +341,15 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
             "kernel": kname + " (persistent, cooperative; NT threads, T targets/thread, TP of them "
                               "paired-reciprocal)",
             "driver": bl.bl_driver_name(lay.h),
-            "peak_basis": f"{nsm} SMs x {MUFU_PER_CLK_SM} MUFU/clk x {sm_max:.0f} MHz "
-                          f"(sm_max_mhz, {peak_src}) / {mufu_per_pair} MUFU per pair",
+            "peak_basis": f"{nsm} SMs x {mufu_clk:g} MUFU/clk (bl_microbench on this box: "
+                          f"{mb_rates[1]:.2f}) x {sm_max:.0f} MHz (sm_max_mhz, {peak_src}) / "
+                          f"{mufu_per_pair} MUFU per pair",
+            "microbench_ops_per_clk_sm": {"ffma": mb_rates[0], "mufu_rcp": mb_rates[1],
+                                          "mufu_rsq": mb_rates[2], "ffma2": mb_rates[3]},
             "frac_at_median_clock": (achieved * mufu_per_pair
-                                     / (nsm * MUFU_PER_CLK_SM * clocks["sm_mhz"] * 1e6)
+                                     / (nsm * mufu_clk * clocks["sm_mhz"] * 1e6)
                                      if clocks.get("sm_mhz") else None),
+            "pipes": load_pipes(name, kname),
         },
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * g.n,
                 "d2h_bytes_per_step": 8 * g.n + 8 * cfg.iters},
@@ -336,8 +367,10 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
             "sample": f"first {k} batch update(s) of iteration 0 of {name} (b={b}), {dt:.1f} s",
         }
     if not args.no_bh:
-        line["bh"] = bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, t_local / args.steps)
+        line["bh"] = bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, t_step)
     line["attraction"] = bench_attraction(lay, d_xy0, params, stream, flush, g, peaks)
+    if args.latency_configs and args.r == -1.0:
+        line["latency"] = bench_latency(args, dev, stream, flush, peak)
     lay.close()
     if args.prof and rank == 0:
         line["phase_profile"] = phase_profile(g, xy0, params, dev, clocks.get("sm_mhz") or sm_max)
@@ -376,6 +409,52 @@ def bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, exact_s):
             "iters_per_sec": cfg.iters / t, "ms_per_step": 1e3 * t, "steps": steps,
             "visits_per_step": visits, "visits_per_sec": visits / t,
             "speedup_vs_exact": exact_s / t, "gpu_launches_per_step": bl.bl_last_launch_count(lay.h)}
+
+
+def bench_latency(args, dev, stream, flush, peak_per_sm_clk):
+    """Secondary objects: the latency-bound configurations (SURVEY.md §8(a)
+    a9: C2, C3 b=256, C4 -- 0.3-1.8 us of roofline work per dependent batch
+    against a grid barrier of ~1.3 us), same timing rules as the headline
+    (L2 flushed, CUDA events on the launching stream, median of the timed
+    steps after warm-ups)."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    from blgen import build_config
+    out = {}
+    for name in args.latency_configs.split(","):
+        if not name:
+            continue
+        g, xy0, cfg = build_config(name)
+        params = dict(iters=cfg.iters, batch=cfg.batch, K=cfg.K, C=cfg.C, step0=cfg.step0,
+                      cooling=cfg.cooling)
+        with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+            d0 = torch.from_numpy(xy0.copy()).to(dev)
+            d = torch.empty_like(d0)
+            for _ in range(3):
+                d.copy_(d0)
+                lay.layout_device(d, stream=stream, **params)
+            torch.cuda.synchronize()
+            ms = []
+            for i in range(max(3, min(args.steps, 5))):
+                d.copy_(d0)
+                flush.fill_(float(i))
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                lay.layout_device(d, stream=stream, **params)
+                b.record(stream)
+                b.synchronize()
+                ms.append(a.elapsed_time(b))
+            t = float(np.median(ms)) / 1e3
+            nb = -(-g.n // cfg.batch)
+            pairs = cfg.iters * g.n * (g.n - 1.0)
+            out[name] = {
+                "iters_per_sec": cfg.iters / t, "ms_per_step": 1e3 * t,
+                "us_per_dependent_batch": 1e6 * t / (cfg.iters * nb),
+                "pair_per_s": pairs / t, "roofline_frac": pairs / t / peak_per_sm_clk,
+                "driver": bl.bl_driver_name(lay.h), "kernel": bl.bl_kernel_name(lay.h),
+                "steps": len(ms), "gpu_launches_per_step": bl.bl_last_launch_count(lay.h)}
+    return out
 
 
 def bench_attraction(lay, d_xy0, params, stream, flush, g, peaks):
@@ -457,6 +536,8 @@ def main(argv=None):
     ap.add_argument("--prof", action="store_true", help="add a phase profile (extra untimed run)")
     ap.add_argument("--no-bh", action="store_true", help="skip the secondary BatchLayoutBH line")
     ap.add_argument("--theta", type=float, default=1.2, help="BatchLayoutBH MAC threshold (P:869)")
+    ap.add_argument("--latency-configs", default="C2,C3b256,C4",
+                    help="secondary latency-bound configs ('' to skip)")
     ap.add_argument("--a", type=float, default=2.0, help="(a, r)-model attraction exponent (P:531)")
     ap.add_argument("--r", type=float, default=-1.0, help="(a, r)-model repulsion exponent")
     args = ap.parse_args(argv)

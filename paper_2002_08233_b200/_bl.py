@@ -133,8 +133,14 @@ def bl_params_default(**overrides) -> bl_params:
 
 
 def bl_create(n: int, rowptr, colidx) -> int:
-    rowptr = np.ascontiguousarray(rowptr, dtype=np.int32)
-    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int32).reshape(-1)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32).reshape(-1)
+    # the C side reads rowptr[0..n] and colidx[0..rowptr[n]) unconditionally
+    if int(n) < 1 or rowptr.size != int(n) + 1:
+        raise BLError(BL_EINVAL, f"rowptr must have n+1 = {int(n) + 1} entries (got {rowptr.size})")
+    if int(rowptr[-1]) != colidx.size:
+        raise BLError(BL_EINVAL, f"colidx must have rowptr[n] = {int(rowptr[-1])} entries "
+                                 f"(got {colidx.size})")
     h = ctypes.c_void_p()
     rc = lib.bl_create(int(n), rowptr.ctypes.data, colidx.ctypes.data if colidx.size else 0,
                        ctypes.byref(h))

@@ -16,9 +16,8 @@
 #include <vector>
 
 #include "../../include/bl.h"
-#include "bl_kernel.cuh"
+#include "bl_ctx.h"
 #include "bl_bh.cuh"
-#include "bl_metrics.cuh"
 #include "bl_cluster.cuh"
 
 #ifndef BL_DEFAULT_NT
@@ -31,65 +30,9 @@
 #define BL_DEFAULT_TP 2
 #endif
 
-struct bl_ctx {
-  int32_t n = 0, nnz = 0;
-  int device = 0, num_sms = 0;
-  int G = 0;  // grid size of the persistent kernel
-  int NT = 512; // threads per CTA
-  int T = 4;  // register-blocked targets per thread
-  int TP = 0; // of which use the paired reciprocal (bl_sweep)
-  // device CSR + items
-  int *d_rowptr = nullptr, *d_colidx = nullptr;
-  int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
-  std::vector<int> item_ptr;  // host copy (per-batch maxima)
-  int n_items = 0;
-  // scratch
-  float2 *d_part = nullptr;
-  size_t part_cap = 0;  // float2 elements
-  float2 *d_pend = nullptr;
-  size_t pend_cap = 0;
-  float2 *d_attr = nullptr;
-  size_t attr_cap = 0;
-  double *d_e_cta = nullptr;
-  double *d_energy = nullptr;
-  size_t energy_cap = 0;
-  int *d_iters_done = nullptr;
-  unsigned *d_bar = nullptr;
-  unsigned long long *d_prof = nullptr;  // BL_PROFILE=1: phase profile
-  bool prof = false;
-  float2 *d_xy_host_path = nullptr;  // staging for bl_layout (host xy)
-  size_t xy_cap = 0;
-  // state of the last call
-  cudaStream_t last_stream = nullptr;
-  int32_t last_iters = 0;
-  bool have_layout = false;
-  int32_t launches = 0;
-  std::string err;
-  char kname[64] = {0};
-  char kname_last[64] = {0};  // the kernel the last layout call launched
-  const char *driver_last = "";  // its batch sequencing (bl_driver_name)
-  // BatchLayoutBH scratch (allocated on first use, sized by n)
-  bool bh_ready = false;
-  unsigned *d_keyA = nullptr, *d_keyB = nullptr, *d_hist = nullptr;
-  int *d_valA = nullptr, *d_valB = nullptr, *d_cnt = nullptr, *d_off = nullptr, *d_blk = nullptr;
-  int *d_nnodes = nullptr;
-  float4 *d_bbox = nullptr, *d_nodeA = nullptr;
-  float2 *d_snap = nullptr, *d_fb = nullptr;
-  size_t fb_cap = 0;
-  int4 *d_nodeB = nullptr, *d_nodeC = nullptr;
-  double2 *d_nsum = nullptr;
-  unsigned long long *d_visits = nullptr;
-  bool last_bh = false;
-  float2 *d_attr_bh = nullptr;
-  unsigned *d_aflag = nullptr;
-  float2 *d_cellf = nullptr;  // BH per-iteration precomputation
-  int *d_nleaf = nullptr, *d_leafv = nullptr;
-  // quality-metric scratch (allocated per call)
-};
-
 static thread_local std::string g_create_err;
 
-static bl_status fail(bl_ctx *h, bl_status s, const char *fmt, ...) {
+bl_status bl_fail(bl_ctx *h, bl_status s, const char *fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -101,14 +44,6 @@ static bl_status fail(bl_ctx *h, bl_status s, const char *fmt, ...) {
     g_create_err = buf;
   return s;
 }
-
-#define BL_CUDA(h, call)                                                                    \
-  do {                                                                                      \
-    cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return fail((h), e_ == cudaErrorMemoryAllocation ? BL_ENOMEM : BL_ECUDA, "%s: %s (%s:%d)", \
-                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                       \
-  } while (0)
 
 extern "C" void bl_params_default(bl_params *p) {
   if (!p) return;
@@ -158,8 +93,8 @@ extern "C" const char *bl_kernel_name(const bl_ctx *h) {
   return h ? (h->kname_last[0] ? h->kname_last : h->kname) : "";
 }
 
-// Not part of the public header: phase profile of the last launch when the
-// context was created with BL_PROFILE=1 (debug aid for bench.py --prof).
+// Debug aid (declared in bl.h): phase profile of the last launch when the
+// context was created with BL_PROFILE=1 (bench.py --prof).
 extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t len) {
   if (!h || !h->d_prof || !out) return 0;
   const int m = std::min<int>(len, 8 + h->G);
@@ -196,24 +131,31 @@ static int chunk4_for(int n, int G) {
 
 
 // Kernel variants (NT threads per CTA, T targets per thread, TP of them
-// paired-reciprocal).  NT x registers is one SM's register file: 512 x 128,
-// 768 x 80, 1024 x 64.
-struct BLVariant {
-  int NT, T, TP;
-  void *fn;
-};
-#define BL_V(NT, T, TP) {NT, T, TP, (void *)bl_layout_kernel<NT, T, TP>}
-static const BLVariant kVariants[] = {
-    BL_V(512, 8, 2),  BL_V(512, 8, 3),  BL_V(512, 8, 4),  BL_V(512, 4, 2),
-    BL_V(768, 6, 2),  BL_V(768, 4, 1),  BL_V(768, 4, 2),
-    BL_V(1024, 4, 1), BL_V(1024, 4, 2), BL_V(1024, 2, 1),
-    BL_V(512, 8, -1),  // general repulsion exponent r (reading C15)
-    BL_V(256, 16, 6),  // 8 warps x 16 targets: best at 2^20 vertices (0.92), not at C5
-};
-#undef BL_V
+// paired-reciprocal), instantiated in bl_exact_*.cu.  NT x registers is one
+// SM's register file: 512 x 128, 768 x 80, 1024 x 64.
+extern const BLVariant bl_exact_v0[], bl_exact_v1[], bl_exact_v2[], bl_exact_v3[], bl_exact_v4[];
+extern const int bl_exact_v0_count, bl_exact_v1_count, bl_exact_v2_count, bl_exact_v3_count,
+    bl_exact_v4_count;
+// v0: <512,8,2> (default), <512,8,-1> (general repulsion exponent r, reading
+// C15); v1: other 512-thread blockings; v2: 768 threads; v3: 1024 threads;
+// v4: <256,16,6> (8 warps x 16 targets: best at 2^20 vertices, not at C5)
+const BLVariant *bl_exact_variants(int *count) {
+  static std::vector<BLVariant> all;
+  if (all.empty()) {
+    const BLVariant *t[] = {bl_exact_v0, bl_exact_v1, bl_exact_v2, bl_exact_v3, bl_exact_v4};
+    const int c[] = {bl_exact_v0_count, bl_exact_v1_count, bl_exact_v2_count, bl_exact_v3_count,
+                     bl_exact_v4_count};
+    for (int k = 0; k < 5; ++k) all.insert(all.end(), t[k], t[k] + c[k]);
+  }
+  *count = (int)all.size();
+  return all.data();
+}
+
 static const BLVariant *find_variant(int NT, int T, int TP) {
-  for (const auto &v : kVariants)
-    if (v.NT == NT && v.T == T && v.TP == TP) return &v;
+  int cnt = 0;
+  const BLVariant *v = bl_exact_variants(&cnt);
+  for (int i = 0; i < cnt; ++i)
+    if (v[i].NT == NT && v[i].T == T && v[i].TP == TP) return &v[i];
   return nullptr;
 }
 
@@ -232,22 +174,22 @@ extern "C" int32_t bl_max_vertices(void) {
 
 extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *colidx,
                                bl_ctx **out) {
-  if (!out) return fail(nullptr, BL_EINVAL, "out is NULL");
+  if (!out) return bl_fail(nullptr, BL_EINVAL, "out is NULL");
   *out = nullptr;
-  if (n < 1) return fail(nullptr, BL_EINVAL, "n must be >= 1 (got %d)", n);
-  if (!rowptr) return fail(nullptr, BL_EINVAL, "rowptr is NULL");
-  if (rowptr[0] != 0) return fail(nullptr, BL_EINVAL, "rowptr[0] != 0");
+  if (n < 1) return bl_fail(nullptr, BL_EINVAL, "n must be >= 1 (got %d)", n);
+  if (!rowptr) return bl_fail(nullptr, BL_EINVAL, "rowptr is NULL");
+  if (rowptr[0] != 0) return bl_fail(nullptr, BL_EINVAL, "rowptr[0] != 0");
   for (int32_t i = 0; i < n; ++i)
-    if (rowptr[i + 1] < rowptr[i]) return fail(nullptr, BL_EINVAL, "rowptr decreases at %d", i);
+    if (rowptr[i + 1] < rowptr[i]) return bl_fail(nullptr, BL_EINVAL, "rowptr decreases at %d", i);
   const int32_t nnz = rowptr[n];
-  if (nnz > 0 && !colidx) return fail(nullptr, BL_EINVAL, "colidx is NULL");
+  if (nnz > 0 && !colidx) return bl_fail(nullptr, BL_EINVAL, "colidx is NULL");
   for (int32_t i = 0; i < n; ++i) {
     for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
       const int32_t j = colidx[k];
-      if (j < 0 || j >= n) return fail(nullptr, BL_EINVAL, "colidx[%d]=%d out of range", k, j);
-      if (j == i) return fail(nullptr, BL_EINVAL, "self loop at vertex %d", i);
+      if (j < 0 || j >= n) return bl_fail(nullptr, BL_EINVAL, "colidx[%d]=%d out of range", k, j);
+      if (j == i) return bl_fail(nullptr, BL_EINVAL, "self loop at vertex %d", i);
       if (k > rowptr[i] && colidx[k - 1] >= j)
-        return fail(nullptr, BL_EINVAL, "row %d not strictly ascending", i);
+        return bl_fail(nullptr, BL_EINVAL, "row %d not strictly ascending", i);
     }
   }
   // symmetry: every (i, j) has (j, i) -- binary search in row j
@@ -255,16 +197,16 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
     for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
       const int32_t j = colidx[k];
       if (!std::binary_search(colidx + rowptr[j], colidx + rowptr[j + 1], i))
-        return fail(nullptr, BL_EINVAL, "not symmetric: (%d,%d) without (%d,%d)", i, j, j, i);
+        return bl_fail(nullptr, BL_EINVAL, "not symmetric: (%d,%d) without (%d,%d)", i, j, j, i);
     }
   }
   const int32_t nmax = bl_max_vertices();
-  if (nmax <= 0) return fail(nullptr, BL_ECUDA, "no usable CUDA device");
+  if (nmax <= 0) return bl_fail(nullptr, BL_ECUDA, "no usable CUDA device");
   if (n > nmax)
-    return fail(nullptr, BL_EINVAL, "n=%d exceeds the resident design limit %d", n, nmax);
+    return bl_fail(nullptr, BL_EINVAL, "n=%d exceeds the resident design limit %d", n, nmax);
 
   bl_ctx *h = new (std::nothrow) bl_ctx();
-  if (!h) return fail(nullptr, BL_ENOMEM, "host allocation failed");
+  if (!h) return bl_fail(nullptr, BL_ENOMEM, "host allocation failed");
   h->n = n;
   h->nnz = nnz;
   auto bad = [&](bl_status s) {
@@ -274,7 +216,7 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   };
   if (cudaGetDevice(&h->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess)
-    return bad(fail(h, BL_ECUDA, "no CUDA device"));
+    return bad(bl_fail(h, BL_ECUDA, "no CUDA device"));
   h->NT = env_int("BL_NT", BL_DEFAULT_NT);
   h->T = env_int("BL_T", BL_DEFAULT_T);
   h->TP = env_int("BL_TP", BL_DEFAULT_TP);
@@ -303,7 +245,7 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
 #define ALLOC(ptr, bytes)                                                  \
   do {                                                                     \
     cudaError_t e_ = cudaMalloc((void **)&(ptr), (bytes));                 \
-    if (e_ != cudaSuccess) return bad(fail(h, BL_ENOMEM, "cudaMalloc %s: %s", #ptr, cudaGetErrorString(e_))); \
+    if (e_ != cudaSuccess) return bad(bl_fail(h, BL_ENOMEM, "cudaMalloc %s: %s", #ptr, cudaGetErrorString(e_))); \
   } while (0)
   ALLOC(h->d_rowptr, sizeof(int) * ((size_t)n + 1));
   ALLOC(h->d_colidx, sizeof(int) * std::max<size_t>(1, nnz));
@@ -321,14 +263,14 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
       cp(h->d_item_ptr, h->item_ptr.data(), sizeof(int) * ((size_t)n + 1)) != cudaSuccess ||
       cp(h->d_item_v, item_v.data(), sizeof(int) * item_v.size()) != cudaSuccess ||
       cp(h->d_item_k0, item_k0.data(), sizeof(int) * item_k0.size()) != cudaSuccess)
-    return bad(fail(h, BL_ECUDA, "CSR upload failed"));
+    return bad(bl_fail(h, BL_ECUDA, "CSR upload failed"));
 
   // grid: one CTA per SM (BL_CTAS_PER_SM overrides), capped by occupancy
   const int per_sm = std::max(1, env_int("BL_CTAS_PER_SM", 1));
   h->G = h->num_sms * per_sm;
   h->prof = env_int("BL_PROFILE", 0) != 0;
   if (h->prof && cudaMalloc((void **)&h->d_prof, sizeof(unsigned long long) * (8 + h->G)) != cudaSuccess)
-    return bad(fail(h, BL_ENOMEM, "profile buffer"));
+    return bad(bl_fail(h, BL_ENOMEM, "profile buffer"));
   *out = h;
   return BL_OK;
 }
@@ -375,23 +317,23 @@ extern "C" void bl_destroy(bl_ctx *h) {
 }
 
 static bl_status check_params(bl_ctx *h, const bl_params *p) {
-  if (!p) return fail(h, BL_EINVAL, "params is NULL");
-  if (p->iters < 0) return fail(h, BL_EINVAL, "iters < 0");
-  if (p->batch < 1) return fail(h, BL_EINVAL, "batch < 1");
-  if (!(p->K > 0.f) || !std::isfinite(p->K)) return fail(h, BL_EINVAL, "K must be > 0");
-  if (!(p->C >= 0.f) || !std::isfinite(p->C)) return fail(h, BL_EINVAL, "C must be >= 0");
-  if (!(p->step0 > 0.0) || !std::isfinite(p->step0)) return fail(h, BL_EINVAL, "step0 must be > 0");
-  if (!(p->cooling > 0.0 && p->cooling <= 1.0)) return fail(h, BL_EINVAL, "cooling must be in (0,1]");
-  if (!(p->tol >= 0.0) || !std::isfinite(p->tol)) return fail(h, BL_EINVAL, "tol must be >= 0");
+  if (!p) return bl_fail(h, BL_EINVAL, "params is NULL");
+  if (p->iters < 0) return bl_fail(h, BL_EINVAL, "iters < 0");
+  if (p->batch < 1) return bl_fail(h, BL_EINVAL, "batch < 1");
+  if (!(p->K > 0.f) || !std::isfinite(p->K)) return bl_fail(h, BL_EINVAL, "K must be > 0");
+  if (!(p->C >= 0.f) || !std::isfinite(p->C)) return bl_fail(h, BL_EINVAL, "C must be >= 0");
+  if (!(p->step0 > 0.0) || !std::isfinite(p->step0)) return bl_fail(h, BL_EINVAL, "step0 must be > 0");
+  if (!(p->cooling > 0.0 && p->cooling <= 1.0)) return bl_fail(h, BL_EINVAL, "cooling must be in (0,1]");
+  if (!(p->tol >= 0.0) || !std::isfinite(p->tol)) return bl_fail(h, BL_EINVAL, "tol must be >= 0");
   if (p->flags & ~(uint32_t)(BL_REPULSE_NEIGHBORS | BL_ATTRACTION_ONLY))
-    return fail(h, BL_EINVAL, "unknown flags");
+    return bl_fail(h, BL_EINVAL, "unknown flags");
   if ((p->flags & BL_ATTRACTION_ONLY) && p->algo != BL_ALGO_EXACT)
-    return fail(h, BL_EINVAL, "BL_ATTRACTION_ONLY needs BL_ALGO_EXACT");
-  if (p->algo != BL_ALGO_EXACT && p->algo != BL_ALGO_BH) return fail(h, BL_EINVAL, "unknown algo");
+    return bl_fail(h, BL_EINVAL, "BL_ATTRACTION_ONLY needs BL_ALGO_EXACT");
+  if (p->algo != BL_ALGO_EXACT && p->algo != BL_ALGO_BH) return bl_fail(h, BL_EINVAL, "unknown algo");
   if (p->algo == BL_ALGO_BH && (!(p->theta >= 0.f) || !std::isfinite(p->theta)))
-    return fail(h, BL_EINVAL, "theta must be >= 0");
-  if (!(p->a >= 0.f && p->a <= 4.f)) return fail(h, BL_EINVAL, "a must be in [0, 4]");
-  if (!(p->r >= -3.f && p->r < 1.f)) return fail(h, BL_EINVAL, "r must be in [-3, 1)");
+    return bl_fail(h, BL_EINVAL, "theta must be >= 0");
+  if (!(p->a >= 0.f && p->a <= 4.f)) return bl_fail(h, BL_EINVAL, "a must be in [0, 4]");
+  if (!(p->r >= -3.f && p->r < 1.f)) return bl_fail(h, BL_EINVAL, "r must be in [-3, 1)");
   return BL_OK;
 }
 
@@ -402,7 +344,7 @@ static bl_status grow(bl_ctx *h, P *&ptr, size_t &cap, size_t need) {
   ptr = nullptr;
   cap = 0;
   cudaError_t e = cudaMalloc((void **)&ptr, need * sizeof(P));
-  if (e != cudaSuccess) return fail(h, BL_ENOMEM, "cudaMalloc scratch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return bl_fail(h, BL_ENOMEM, "cudaMalloc scratch: %s", cudaGetErrorString(e));
   cap = need;
   return BL_OK;
 }
@@ -519,14 +461,16 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
                    : k.pipelined      ? "pipelined"
                                       : "two-barrier";
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
+  if (e != cudaSuccess) return bl_fail(h, BL_ECUDA, "smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
   int occ = 0;
   BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, vt->NT, smem));
   if (occ * h->num_sms < G)
-    return fail(h, BL_ECUDA, "cooperative grid %d exceeds residency %d x %d SMs", G, occ, h->num_sms);
+    return bl_fail(h, BL_ECUDA, "cooperative grid %d exceeds residency %d x %d SMs", G, occ, h->num_sms);
 
   BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
-  BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+  // forces mode never writes iters_done: leave the last layout call's count
+  // (and its energy trace) to bl_energy
+  if (!forces_mode) BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
   if (h->d_prof) BL_CUDA(h, cudaMemsetAsync(h->d_prof, 0, sizeof(unsigned long long) * (8 + G), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(vt->NT), args, smem, st));
@@ -545,7 +489,7 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
 #define ALLOC(ptr, cnt)                                                                       \
   do {                                                                                        \
     cudaError_t e_ = cudaMalloc((void **)&(ptr), sizeof(*(ptr)) * (size_t)(cnt));             \
-    if (e_ != cudaSuccess) return fail(h, BL_ENOMEM, "cudaMalloc %s: %s", #ptr, cudaGetErrorString(e_)); \
+    if (e_ != cudaSuccess) return bl_fail(h, BL_ENOMEM, "cudaMalloc %s: %s", #ptr, cudaGetErrorString(e_)); \
   } while (0)
     ALLOC(h->d_keyA, n);
     ALLOC(h->d_keyB, n);
@@ -629,19 +573,19 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.bar = h->d_bar;
   k.f_out = f_out;
   k.visits = h->d_visits;
-  void *kfn = (void *)bl_bh_kernel<BH_NT>;
-  const size_t smem = sizeof(BHShared);
+  void *kfn = bl_bh_kernel_fn();
+  const size_t smem = bl_bh_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return fail(h, BL_ECUDA, "bh smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
+  if (e != cudaSuccess) return bl_fail(h, BL_ECUDA, "bh smem attribute (%zu B): %s", smem, cudaGetErrorString(e));
   int occ = 0;
-  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, BH_NT, smem));
-  if (occ < 1) return fail(h, BL_ECUDA, "bh kernel does not fit an SM");
+  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, bl_bh_threads(), smem));
+  if (occ < 1) return bl_fail(h, BL_ECUDA, "bh kernel does not fit an SM");
   BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
-  BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+  if (!forces_mode) BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
   BL_CUDA(h, cudaMemsetAsync(h->d_visits, 0, sizeof(unsigned long long) * G, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_aflag, 0, sizeof(unsigned) * std::max(1, h->n_items), st));
   void *args[] = {&k};
-  BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(BH_NT), args, smem, st));
+  BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(bl_bh_threads()), args, smem, st));
   h->launches = 1;
   h->last_bh = true;
   return BL_OK;
@@ -674,15 +618,12 @@ static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
   model_codes(p, &amode, &rmode, &a_half, &r_half);
   // cluster size: 16 (non-portable) if the device can co-schedule it, else 8
   int CS = 0;
-  void *fns[3][2] = {{(void *)bl_cluster_kernel<1, 0>, (void *)bl_cluster_kernel<1, -1>},
-                     {(void *)bl_cluster_kernel<2, 0>, (void *)bl_cluster_kernel<2, -1>},
-                     {(void *)bl_cluster_kernel<4, 0>, (void *)bl_cluster_kernel<4, -1>}};
   const int tsel = env_int("BL_CLUSTER_T", 0);  // 0: by slice size
   for (int cs : {16, 8}) {
     const int sl = (b + cs - 1) / cs;
     if (sl > BLC_SLICE_MAX) continue;
     const int tt = tsel == 1 ? 0 : tsel == 2 ? 1 : tsel == 4 ? 2 : (sl <= 16 ? 0 : 1);
-    void *kfn = fns[tt][rmode ? 1 : 0];
+    void *kfn = bl_cluster_kernel_fn(tt, rmode);
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       continue;
     if (cs > 8 && cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -746,7 +687,7 @@ static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
 }
 
 extern "C" bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits) {
-  if (!h || !visits) return fail(h, BL_EINVAL, "NULL argument");
+  if (!h || !visits) return bl_fail(h, BL_EINVAL, "NULL argument");
   *visits = 0;
   if (!h->last_bh || !h->d_visits) return BL_OK;
   BL_CUDA(h, cudaStreamSynchronize(h->last_stream));
@@ -758,15 +699,16 @@ extern "C" bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits) {
 }
 
 extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p, void *cuda_stream) {
-  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  if (!h) return bl_fail(nullptr, BL_EINVAL, "handle is NULL");
   h->launches = 0;
   bl_status s = check_params(h, p);
   if (s != BL_OK) return s;
-  if (!d_xy) return fail(h, BL_EINVAL, "d_xy is NULL");
-  if (((uintptr_t)d_xy) & 7) return fail(h, BL_EINVAL, "d_xy must be 8-byte aligned");
-  if (p->flags & BL_ATTRACTION_ONLY) return fail(h, BL_EINVAL, "BL_ATTRACTION_ONLY is for bl_forces");
+  if (!d_xy) return bl_fail(h, BL_EINVAL, "d_xy is NULL");
+  if (((uintptr_t)d_xy) & 7) return bl_fail(h, BL_EINVAL, "d_xy must be 8-byte aligned");
+  if (p->flags & BL_ATTRACTION_ONLY) return bl_fail(h, BL_EINVAL, "BL_ATTRACTION_ONLY is for bl_forces");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   h->last_stream = st;
+  h->layout_stream = st;
   h->last_iters = p->iters;
   if (p->iters == 0) {
     h->have_layout = false;
@@ -789,12 +731,12 @@ extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p
 }
 
 extern "C" bl_status bl_layout(bl_ctx *h, float *xy, const bl_params *p, int32_t *iters_done) {
-  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  if (!h) return bl_fail(nullptr, BL_EINVAL, "handle is NULL");
   bl_status s = check_params(h, p);
   if (s != BL_OK) return s;
-  if (!xy) return fail(h, BL_EINVAL, "xy is NULL");
+  if (!xy) return bl_fail(h, BL_EINVAL, "xy is NULL");
   for (int32_t i = 0; i < 2 * h->n; ++i)
-    if (!std::isfinite(xy[i])) return fail(h, BL_EINVAL, "non-finite coordinate at %d", i);
+    if (!std::isfinite(xy[i])) return bl_fail(h, BL_EINVAL, "non-finite coordinate at %d", i);
   if ((s = grow(h, h->d_xy_host_path, h->xy_cap, (size_t)h->n)) != BL_OK) return s;
   cudaStream_t st = nullptr;
   BL_CUDA(h, cudaMemcpyAsync(h->d_xy_host_path, xy, sizeof(float2) * h->n, cudaMemcpyHostToDevice, st));
@@ -813,10 +755,10 @@ extern "C" bl_status bl_layout(bl_ctx *h, float *xy, const bl_params *p, int32_t
 
 extern "C" bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t trace_len,
                                int32_t *n_written, int32_t *iters_done) {
-  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
-  if (trace_len < 0) return fail(h, BL_EINVAL, "trace_len < 0");
-  if (!h->have_layout) return fail(h, BL_ESTATE, "no layout call has run an iteration");
-  BL_CUDA(h, cudaStreamSynchronize(h->last_stream));
+  if (!h) return bl_fail(nullptr, BL_EINVAL, "handle is NULL");
+  if (trace_len < 0) return bl_fail(h, BL_EINVAL, "trace_len < 0");
+  if (!h->have_layout) return bl_fail(h, BL_ESTATE, "no layout call has run an iteration");
+  BL_CUDA(h, cudaStreamSynchronize(h->layout_stream));
   int d = 0;
   BL_CUDA(h, cudaMemcpy(&d, h->d_iters_done, sizeof(int), cudaMemcpyDeviceToHost));
   if (iters_done) *iters_done = d;
@@ -828,7 +770,7 @@ extern "C" bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t
     if (n_written) *n_written = m;
   }
   if (e_last) {
-    if (avail == 0) return fail(h, BL_ESTATE, "no completed iteration");
+    if (avail == 0) return bl_fail(h, BL_ESTATE, "no completed iteration");
     BL_CUDA(h, cudaMemcpy(e_last, h->d_energy + (avail - 1), sizeof(double), cudaMemcpyDeviceToHost));
   }
   return BL_OK;
@@ -836,13 +778,13 @@ extern "C" bl_status bl_energy(bl_ctx *h, double *e_last, double *trace, int32_t
 
 extern "C" bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int32_t count,
                                float *d_f_out, const bl_params *p, void *cuda_stream) {
-  if (!h) return fail(nullptr, BL_EINVAL, "handle is NULL");
+  if (!h) return bl_fail(nullptr, BL_EINVAL, "handle is NULL");
   h->launches = 0;
   bl_status s = check_params(h, p);
   if (s != BL_OK) return s;
-  if (!d_xy || !d_f_out) return fail(h, BL_EINVAL, "NULL pointer");
+  if (!d_xy || !d_f_out) return bl_fail(h, BL_EINVAL, "NULL pointer");
   if (first < 0 || count < 0 || first > h->n - count)
-    return fail(h, BL_EINVAL, "range [%d, %d+%d) outside [0, %d)", first, first, count, h->n);
+    return bl_fail(h, BL_EINVAL, "range [%d, %d+%d) outside [0, %d)", first, first, count, h->n);
   if (count == 0) return BL_OK;
   h->last_stream = (cudaStream_t)cuda_stream;
   h->last_bh = false;
@@ -854,139 +796,3 @@ extern "C" bl_status bl_forces(bl_ctx *h, const float *d_xy, int32_t first, int3
                 reinterpret_cast<float2 *>(d_f_out));
 }
 
-// ------------------------------------------------------------------ metrics
-// Quality metrics of §3.7 (csrc/bl_metrics.cuh).  Synchronous on the stream.
-namespace {
-struct DevBuf {
-  void *p = nullptr;
-  ~DevBuf() { cudaFree(p); }
-  template <typename T>
-  T *as() { return reinterpret_cast<T *>(p); }
-};
-}  // namespace
-
-#define BLM_ALLOC(h, buf, bytes)                                                             \
-  do {                                                                                       \
-    cudaError_t e_ = cudaMalloc(&(buf).p, (bytes));                                          \
-    if (e_ != cudaSuccess) return fail((h), BL_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e_)); \
-  } while (0)
-
-extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu, void *cuda_stream) {
-  if (!h || !d_xy || !eu) return fail(h, BL_EINVAL, "NULL argument");
-  cudaStream_t st = (cudaStream_t)cuda_stream;
-  const int nb = 4 * h->num_sms;
-  DevBuf part, stats;
-  BLM_ALLOC(h, part, sizeof(double2) * nb);
-  BLM_ALLOC(h, stats, sizeof(double) * 8);
-  const float2 *xy = reinterpret_cast<const float2 *>(d_xy);
-  for (int pass = 0; pass < 2; ++pass) {
-    blm_eu_pass<<<nb, BLM_NT, 0, st>>>(h->d_rowptr, h->d_colidx, xy, h->n, pass, stats.as<double>(),
-                                        part.as<double2>());
-    blm_reduce_parts<<<1, 32, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
-  }
-  BL_CUDA(h, cudaGetLastError());
-  BL_CUDA(h, cudaMemcpyAsync(eu, stats.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
-  BL_CUDA(h, cudaStreamSynchronize(st));
-  h->launches = 4;
-  return BL_OK;
-}
-
-extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sources, int32_t nsrc,
-                               double *stress, double *scale, long long *pairs,
-                               long long *unreachable, void *cuda_stream) {
-  if (!h || !d_xy || !stress) return fail(h, BL_EINVAL, "NULL argument");
-  const int n = h->n;
-  if (sources) {
-    if (nsrc < 1) return fail(h, BL_EINVAL, "nsrc < 1");
-    for (int32_t t = 0; t < nsrc; ++t)
-      if (sources[t] < 0 || sources[t] >= n) return fail(h, BL_EINVAL, "source %d out of range", sources[t]);
-  } else {
-    nsrc = n;
-  }
-  cudaStream_t st = (cudaStream_t)cuda_stream;
-  std::vector<int32_t> src(nsrc);
-  for (int32_t t = 0; t < nsrc; ++t) src[t] = sources ? sources[t] : t;
-  int occ = 0;
-  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blm_stress_kernel, BLM_NT, 0));
-  const int G = h->num_sms * std::max(1, std::min(occ, 4));
-  DevBuf d_src, vis, fa, fb, aA, aB, aN, flag, bar, out4, outN;
-  BLM_ALLOC(h, d_src, sizeof(int32_t) * nsrc);
-  BLM_ALLOC(h, vis, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, fa, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, fb, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, aA, sizeof(double) * G * BLM_NT);
-  BLM_ALLOC(h, aB, sizeof(double) * G * BLM_NT);
-  BLM_ALLOC(h, aN, sizeof(unsigned long long) * G * BLM_NT);
-  BLM_ALLOC(h, flag, sizeof(int) * 3);
-  BLM_ALLOC(h, bar, sizeof(unsigned));
-  BLM_ALLOC(h, out4, sizeof(double) * 4);
-  BLM_ALLOC(h, outN, sizeof(unsigned long long));
-  BL_CUDA(h, cudaMemcpyAsync(d_src.p, src.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st));
-  BL_CUDA(h, cudaMemsetAsync(bar.p, 0, sizeof(unsigned), st));
-  BLMStressParams k{};
-  k.n = n;
-  k.nsrc = nsrc;
-  k.rowptr = h->d_rowptr;
-  k.colidx = h->d_colidx;
-  k.xy = reinterpret_cast<const float2 *>(d_xy);
-  k.sources = d_src.as<int>();
-  k.vis = vis.as<unsigned long long>();
-  k.frontA = fa.as<unsigned long long>();
-  k.frontB = fb.as<unsigned long long>();
-  k.accA = aA.as<double>();
-  k.accB = aB.as<double>();
-  k.accN = aN.as<unsigned long long>();
-  k.flag = flag.as<int>();
-  k.bar = bar.as<unsigned>();
-  void *args[] = {&k};
-  BL_CUDA(h, cudaLaunchCooperativeKernel((void *)blm_stress_kernel, dim3(G), dim3(BLM_NT), args, 0, st));
-  blm_stress_reduce<<<1, 32, 0, st>>>(k.accA, k.accB, k.accN, G * BLM_NT, out4.as<double>(),
-                                      outN.as<unsigned long long>());
-  BL_CUDA(h, cudaGetLastError());
-  double o[4];
-  unsigned long long N = 0;
-  BL_CUDA(h, cudaMemcpyAsync(o, out4.p, sizeof o, cudaMemcpyDeviceToHost, st));
-  BL_CUDA(h, cudaMemcpyAsync(&N, outN.p, sizeof N, cudaMemcpyDeviceToHost, st));
-  BL_CUDA(h, cudaStreamSynchronize(st));
-  *stress = o[0];
-  if (scale) *scale = o[1];
-  if (pairs) *pairs = (long long)N;
-  if (unreachable) *unreachable = (long long)nsrc * (n - 1) - (long long)N;
-  h->launches = 2;
-  return BL_OK;
-}
-
-extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
-                                                  const int32_t *queries, int32_t nq, double *np,
-                                                  int32_t *counted, void *cuda_stream) {
-  if (!h || !d_xy || !np) return fail(h, BL_EINVAL, "NULL argument");
-  const int n = h->n;
-  if (queries) {
-    if (nq < 1) return fail(h, BL_EINVAL, "nq < 1");
-    for (int32_t t = 0; t < nq; ++t)
-      if (queries[t] < 0 || queries[t] >= n) return fail(h, BL_EINVAL, "query %d out of range", queries[t]);
-  } else {
-    nq = n;
-  }
-  cudaStream_t st = (cudaStream_t)cuda_stream;
-  DevBuf d_q, jac, out, cnt;
-  if (queries) {
-    BLM_ALLOC(h, d_q, sizeof(int32_t) * nq);
-    BL_CUDA(h, cudaMemcpyAsync(d_q.p, queries, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st));
-  }
-  BLM_ALLOC(h, jac, sizeof(double) * nq);
-  BLM_ALLOC(h, out, sizeof(double));
-  BLM_ALLOC(h, cnt, sizeof(int));
-  blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx,
-                                                reinterpret_cast<const float2 *>(d_xy), n,
-                                                queries ? d_q.as<int>() : nullptr, nq, jac.as<double>());
-  blm_np_reduce<<<1, 32, 0, st>>>(jac.as<double>(), nq, out.as<double>(), cnt.as<int>());
-  BL_CUDA(h, cudaGetLastError());
-  int c = 0;
-  BL_CUDA(h, cudaMemcpyAsync(np, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-  BL_CUDA(h, cudaMemcpyAsync(&c, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  BL_CUDA(h, cudaStreamSynchronize(st));
-  if (counted) *counted = c;
-  h->launches = 2;
-  return BL_OK;
-}

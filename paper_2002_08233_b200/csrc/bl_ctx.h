@@ -1,0 +1,91 @@
+// bl_ctx.h -- the context behind the opaque bl_ctx handle of include/bl.h,
+// shared by the host translation units of libbl (bl_api.cu, bl_metrics.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bl.h"
+#include "bl_kernel.cuh"
+
+struct bl_ctx {
+  int32_t n = 0, nnz = 0;
+  int device = 0, num_sms = 0;
+  int G = 0;  // grid size of the persistent kernel
+  int NT = 512; // threads per CTA
+  int T = 4;  // register-blocked targets per thread
+  int TP = 0; // of which use the paired reciprocal (bl_sweep)
+  // device CSR + items
+  int *d_rowptr = nullptr, *d_colidx = nullptr;
+  int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
+  std::vector<int> item_ptr;  // host copy (per-batch maxima)
+  int n_items = 0;
+  // scratch
+  float2 *d_part = nullptr;
+  size_t part_cap = 0;  // float2 elements
+  float2 *d_pend = nullptr;
+  size_t pend_cap = 0;
+  float2 *d_attr = nullptr;
+  size_t attr_cap = 0;
+  double *d_e_cta = nullptr;
+  double *d_energy = nullptr;
+  size_t energy_cap = 0;
+  int *d_iters_done = nullptr;
+  unsigned *d_bar = nullptr;
+  unsigned long long *d_prof = nullptr;  // BL_PROFILE=1: phase profile
+  bool prof = false;
+  float2 *d_xy_host_path = nullptr;  // staging for bl_layout (host xy)
+  size_t xy_cap = 0;
+  // state of the last call
+  cudaStream_t last_stream = nullptr;    // stream of the last call (any kind)
+  cudaStream_t layout_stream = nullptr;  // stream of the last layout call (bl_energy)
+  int32_t last_iters = 0;
+  bool have_layout = false;
+  int32_t launches = 0;
+  std::string err;
+  char kname[64] = {0};
+  char kname_last[64] = {0};  // the kernel the last layout call launched
+  const char *driver_last = "";  // its batch sequencing (bl_driver_name)
+  // BatchLayoutBH scratch (allocated on first use, sized by n)
+  bool bh_ready = false;
+  unsigned *d_keyA = nullptr, *d_keyB = nullptr, *d_hist = nullptr;
+  int *d_valA = nullptr, *d_valB = nullptr, *d_cnt = nullptr, *d_off = nullptr, *d_blk = nullptr;
+  int *d_nnodes = nullptr;
+  float4 *d_bbox = nullptr, *d_nodeA = nullptr;
+  float2 *d_snap = nullptr, *d_fb = nullptr;
+  size_t fb_cap = 0;
+  int4 *d_nodeB = nullptr, *d_nodeC = nullptr;
+  double2 *d_nsum = nullptr;
+  unsigned long long *d_visits = nullptr;
+  bool last_bh = false;
+  float2 *d_attr_bh = nullptr;
+  unsigned *d_aflag = nullptr;
+  float2 *d_cellf = nullptr;  // BH per-iteration precomputation
+  int *d_nleaf = nullptr, *d_leafv = nullptr;
+  // quality-metric scratch (allocated per call)
+};
+
+
+// record the message (on h, or for bl_create) and return s
+bl_status bl_fail(bl_ctx *h, bl_status s, const char *fmt, ...);
+
+#define BL_CUDA(h, call)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return bl_fail((h), e_ == cudaErrorMemoryAllocation ? BL_ENOMEM : BL_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+  } while (0)
+
+
+// kernel tables: each lives in its own translation unit (parallel builds)
+struct BLVariant {
+  int NT, T, TP;
+  void *fn;
+};
+const BLVariant *bl_exact_variants(int *count);     // bl_exact_*.cu
+void *bl_bh_kernel_fn();                            // bl_bh.cu
+size_t bl_bh_smem_bytes();
+int bl_bh_threads();
+void *bl_cluster_kernel_fn(int tt, int rmode);      // bl_cluster.cu

@@ -1013,7 +1013,7 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
   const int G = gridDim.x, c = blockIdx.x;
   const int nb = p.nb;
   const long long ptot = (long long)p.iters * nb;
-  const bool mb_stop = p.max_batches > 0 && p.max_batches < ptot;
+  const bool mb_stop = p.max_batches > 0 && p.max_batches <= ptot;  // == ptot: as the oracle, iters - 1 done
   const int P = mb_stop ? p.max_batches : (int)ptot;
   double step_u = p.step0;
   if (threadIdx.x == 0) {
@@ -1148,7 +1148,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int nb = p.nb;
   const long long ptot = (long long)p.iters * nb;
-  const bool mb_stop = p.max_batches > 0 && p.max_batches < ptot;
+  const bool mb_stop = p.max_batches > 0 && p.max_batches <= ptot;  // == ptot: as the oracle, iters - 1 done
   const int P = mb_stop ? p.max_batches : (int)ptot;
   const int half = p.red_cap / 2;  // red slots per phase parity
   const volatile BLShared &vs = sh;

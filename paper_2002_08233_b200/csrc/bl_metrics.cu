@@ -1,0 +1,148 @@
+// bl_metrics.cu -- host side of the §3.7 quality metrics of the
+// C-ABI (include/bl.h); kernels in bl_metrics.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "bl_ctx.h"
+#include "bl_metrics.cuh"
+
+#define fail bl_fail
+
+// ------------------------------------------------------------------ metrics
+// Quality metrics of §3.7 (csrc/bl_metrics.cuh).  Synchronous on the stream.
+namespace {
+struct DevBuf {
+  void *p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  template <typename T>
+  T *as() { return reinterpret_cast<T *>(p); }
+};
+}  // namespace
+
+#define BLM_ALLOC(h, buf, bytes)                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = cudaMalloc(&(buf).p, (bytes));                                          \
+    if (e_ != cudaSuccess) return bl_fail((h), BL_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu, void *cuda_stream) {
+  if (!h || !d_xy || !eu) return bl_fail(h, BL_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int nb = 4 * h->num_sms;
+  DevBuf part, stats;
+  BLM_ALLOC(h, part, sizeof(double2) * nb);
+  BLM_ALLOC(h, stats, sizeof(double) * 8);
+  const float2 *xy = reinterpret_cast<const float2 *>(d_xy);
+  for (int pass = 0; pass < 2; ++pass) {
+    blm_eu_pass<<<nb, BLM_NT, 0, st>>>(h->d_rowptr, h->d_colidx, xy, h->n, pass, stats.as<double>(),
+                                        part.as<double2>());
+    blm_reduce_parts<<<1, 32, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
+  }
+  BL_CUDA(h, cudaGetLastError());
+  BL_CUDA(h, cudaMemcpyAsync(eu, stats.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaStreamSynchronize(st));
+  h->launches = 4;
+  return BL_OK;
+}
+
+extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sources, int32_t nsrc,
+                               double *stress, double *scale, long long *pairs,
+                               long long *unreachable, void *cuda_stream) {
+  if (!h || !d_xy || !stress) return bl_fail(h, BL_EINVAL, "NULL argument");
+  const int n = h->n;
+  if (sources) {
+    if (nsrc < 1) return bl_fail(h, BL_EINVAL, "nsrc < 1");
+    for (int32_t t = 0; t < nsrc; ++t)
+      if (sources[t] < 0 || sources[t] >= n) return bl_fail(h, BL_EINVAL, "source %d out of range", sources[t]);
+  } else {
+    nsrc = n;
+  }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  std::vector<int32_t> src(nsrc);
+  for (int32_t t = 0; t < nsrc; ++t) src[t] = sources ? sources[t] : t;
+  int occ = 0;
+  BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blm_stress_kernel, BLM_NT, 0));
+  const int G = h->num_sms * std::max(1, std::min(occ, 4));
+  DevBuf d_src, vis, fa, fb, aA, aB, aN, flag, bar, out4, outN;
+  BLM_ALLOC(h, d_src, sizeof(int32_t) * nsrc);
+  BLM_ALLOC(h, vis, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, fa, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, fb, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, aA, sizeof(double) * G * BLM_NT);
+  BLM_ALLOC(h, aB, sizeof(double) * G * BLM_NT);
+  BLM_ALLOC(h, aN, sizeof(unsigned long long) * G * BLM_NT);
+  BLM_ALLOC(h, flag, sizeof(int) * 3);
+  BLM_ALLOC(h, bar, sizeof(unsigned));
+  BLM_ALLOC(h, out4, sizeof(double) * 4);
+  BLM_ALLOC(h, outN, sizeof(unsigned long long));
+  BL_CUDA(h, cudaMemcpyAsync(d_src.p, src.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st));
+  BL_CUDA(h, cudaMemsetAsync(bar.p, 0, sizeof(unsigned), st));
+  BLMStressParams k{};
+  k.n = n;
+  k.nsrc = nsrc;
+  k.rowptr = h->d_rowptr;
+  k.colidx = h->d_colidx;
+  k.xy = reinterpret_cast<const float2 *>(d_xy);
+  k.sources = d_src.as<int>();
+  k.vis = vis.as<unsigned long long>();
+  k.frontA = fa.as<unsigned long long>();
+  k.frontB = fb.as<unsigned long long>();
+  k.accA = aA.as<double>();
+  k.accB = aB.as<double>();
+  k.accN = aN.as<unsigned long long>();
+  k.flag = flag.as<int>();
+  k.bar = bar.as<unsigned>();
+  void *args[] = {&k};
+  BL_CUDA(h, cudaLaunchCooperativeKernel((void *)blm_stress_kernel, dim3(G), dim3(BLM_NT), args, 0, st));
+  blm_stress_reduce<<<1, 32, 0, st>>>(k.accA, k.accB, k.accN, G * BLM_NT, out4.as<double>(),
+                                      outN.as<unsigned long long>());
+  BL_CUDA(h, cudaGetLastError());
+  double o[4];
+  unsigned long long N = 0;
+  BL_CUDA(h, cudaMemcpyAsync(o, out4.p, sizeof o, cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaMemcpyAsync(&N, outN.p, sizeof N, cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaStreamSynchronize(st));
+  *stress = o[0];
+  if (scale) *scale = o[1];
+  if (pairs) *pairs = (long long)N;
+  if (unreachable) *unreachable = (long long)nsrc * (n - 1) - (long long)N;
+  h->launches = 2;
+  return BL_OK;
+}
+
+extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
+                                                  const int32_t *queries, int32_t nq, double *np,
+                                                  int32_t *counted, void *cuda_stream) {
+  if (!h || !d_xy || !np) return bl_fail(h, BL_EINVAL, "NULL argument");
+  const int n = h->n;
+  if (queries) {
+    if (nq < 1) return bl_fail(h, BL_EINVAL, "nq < 1");
+    for (int32_t t = 0; t < nq; ++t)
+      if (queries[t] < 0 || queries[t] >= n) return bl_fail(h, BL_EINVAL, "query %d out of range", queries[t]);
+  } else {
+    nq = n;
+  }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  DevBuf d_q, jac, out, cnt;
+  if (queries) {
+    BLM_ALLOC(h, d_q, sizeof(int32_t) * nq);
+    BL_CUDA(h, cudaMemcpyAsync(d_q.p, queries, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st));
+  }
+  BLM_ALLOC(h, jac, sizeof(double) * nq);
+  BLM_ALLOC(h, out, sizeof(double));
+  BLM_ALLOC(h, cnt, sizeof(int));
+  blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx,
+                                                reinterpret_cast<const float2 *>(d_xy), n,
+                                                queries ? d_q.as<int>() : nullptr, nq, jac.as<double>());
+  blm_np_reduce<<<1, 32, 0, st>>>(jac.as<double>(), nq, out.as<double>(), cnt.as<int>());
+  BL_CUDA(h, cudaGetLastError());
+  int c = 0;
+  BL_CUDA(h, cudaMemcpyAsync(np, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaMemcpyAsync(&c, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaStreamSynchronize(st));
+  if (counted) *counted = c;
+  h->launches = 2;
+  return BL_OK;
+}

@@ -19,12 +19,16 @@ class BatchLayout:
         done = _bl.bl_layout(self.h, xy, _bl.bl_params_default(**params))
         return xy, done
 
+    def _check_device_xy(self, d_xy):
+        import torch
+        if not (isinstance(d_xy, torch.Tensor) and d_xy.is_cuda and d_xy.dtype == torch.float32
+                and d_xy.is_contiguous() and d_xy.numel() == 2 * self.n):
+            raise TypeError("d_xy must be a contiguous float32 CUDA tensor with 2n elements")
+
     # -- device path: torch CUDA float32 (n, 2) tensor updated in place
     def layout_device(self, d_xy, stream=None, **params):
         import torch
-        if not (d_xy.is_cuda and d_xy.dtype == torch.float32 and d_xy.is_contiguous()
-                and d_xy.numel() == 2 * self.n):
-            raise TypeError("d_xy must be a contiguous float32 CUDA tensor with 2n elements")
+        self._check_device_xy(d_xy)
         if stream is None:
             stream = torch.cuda.current_stream(d_xy.device)
         _bl.bl_layout_device(self.h, d_xy, _bl.bl_params_default(**params), stream)
@@ -34,6 +38,7 @@ class BatchLayout:
 
     def forces(self, d_xy, first: int = 0, count: int | None = None, stream=None, **params):
         import torch
+        self._check_device_xy(d_xy)
         if count is None:
             count = self.n - first
         out = torch.empty((max(count, 1), 2), dtype=torch.float32, device=d_xy.device)

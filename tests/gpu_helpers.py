@@ -1,9 +1,48 @@
 """Shared helpers for the -m gpu tests: run the CUDA path through the C-ABI
-and compare with the oracle.  Tolerances are derived in DESIGN.md §6."""
+and compare with the oracle.  Tolerances are derived in DESIGN.md §6.
+
+BL_PARITY_LOG=<file>: every comparison appends one JSON line (what, the
+measured error, the gate) -- the margins behind DESIGN.md §6's table."""
+import json
+import os
+
 import numpy as np
 
-# north star: "max position error <= 1e-4 x layout extent (fp32)"
+# north star: "max position error <= 1e-4 x layout extent (fp32)" -- one full
+# iteration and shadowed iterations (chaotic amplification inside the
+# iteration)
 POS_TOL = 1e-4
+# one batch update: no propagation, error = Step x the direction error of
+# fp32 forces
+POS_TOL_BATCH = 1e-5
+# energy of one batch / one iteration / one shadowed iteration, relative
+# (fp32 chunked sums, fp64 energy accumulation)
+E_TOL = 1e-6
+# the same with (a, r)-model powers through lg2/ex2.approx
+E_TOL_POW = 1e-5
+U32 = 2.0 ** -24  # fp32 unit roundoff
+
+
+def _log(what, kind, value, gate):
+    path = os.environ.get("BL_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0],
+                                 "what": what, "kind": kind, "value": float(value),
+                                 "gate": float(gate)}) + "\n")
+
+
+def assert_energy_close(got, ref, tol=E_TOL, what=""):
+    """|E_gpu - E_oracle| <= tol x E_oracle for every entry (E = 0 exactly
+    when every force is 0, compared exactly)."""
+    got = np.atleast_1d(np.asarray(got, np.float64))
+    ref = np.atleast_1d(np.asarray(ref, np.float64))
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    rel = np.where(ref > 0, np.abs(got - ref) / np.where(ref > 0, ref, 1.0), np.abs(got - ref))
+    worst = float(rel.max()) if rel.size else 0.0
+    _log(what, "energy_rel", worst, tol)
+    assert worst <= tol, f"{what}: energy rel. diff {worst:.3e} > {tol:g} ({got} vs {ref})"
+    return worst
 
 
 def extent(xy):
@@ -49,9 +88,12 @@ def gpu_forces(g, xy, first=0, count=None, with_visits=False, **params):
         return out
 
 
-def assert_positions_close(got, ref, tol=POS_TOL, what=""):
-    ext = extent(ref)
+def assert_positions_close(got, ref, tol=POS_TOL, what="", ext=None):
+    """max |got - ref| <= tol x extent (reading C13: the extent of the
+    reference layout, or of the whole layout `ext` when comparing a part)."""
+    ext = extent(ref) if ext is None else ext
     err = float(np.abs(np.asarray(got, np.float64) - ref).max())
+    _log(what, "pos_over_extent", err / ext if ext > 0 else err, tol)
     assert err <= tol * ext, f"{what}: max |dxy| = {err:.3e} > {tol:g} x extent {ext:.4g}"
     return err / ext
 
@@ -69,8 +111,8 @@ def shadow_check(g, xy0, iters, oracle_layout, tol=POS_TOL, **params):
         p = dict(params, iters=1, step0=step)
         got, tr, _ = gpu_layout(g, state, **p)
         ref, E, _ = oracle_layout(g, state, p)
-        worst = max(worst, assert_positions_close(got, ref, tol, what=f"iteration {t}"))
-        assert abs(tr[0] - E[0]) <= 1e-3 * E[0] + 1e-30, (t, tr[0], E[0])
+        worst = max(worst, assert_positions_close(got, ref, tol, what=f"shadowed iteration {t}"))
+        assert_energy_close(tr[:1], E[:1], what=f"shadowed iteration {t}")
         state = got
         step = step * cooling
     return worst

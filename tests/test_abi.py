@@ -97,3 +97,20 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("no CPU fallback", ""), f
+
+
+@pytest.mark.parametrize("case", [
+    ("rowptr_short", 3, [0, 1, 2], [1, 0]),          # n + 1 = 4 entries expected
+    ("rowptr_long", 2, [0, 1, 2, 2], [1, 0]),
+    ("colidx_short", 2, [0, 1, 2], [1]),             # rowptr[n] = 2 entries expected
+    ("colidx_long", 2, [0, 1, 2], [1, 0, 1]),
+])
+def test_binding_rejects_missized_csr_before_the_c_call(case):
+    """The C side reads rowptr[0..n] and colidx[0..rowptr[n]) unconditionally;
+    the binding checks the array sizes first (no out-of-bounds host read)."""
+    import paper_2002_08233_b200 as bl
+    _, n, rp, ci = case
+    with pytest.raises(bl.BLError) as ei:
+        bl.bl_create(n, np.array(rp, np.int32), np.array(ci, np.int32))
+    assert ei.value.status == bl.BL_EINVAL
+    assert "entries" in str(ei.value)

@@ -14,7 +14,9 @@ import pytest
 import oracle
 from blgen import (build_config, cycle_graph, edges_to_csr, grid_graph, rmat_graph, star_graph,
                    uniform_coords)
-from tests.gpu_helpers import assert_positions_close, extent, gpu_forces, gpu_layout, shadow_check
+from tests.gpu_helpers import (POS_TOL, POS_TOL_BATCH, U32, assert_energy_close,
+                               assert_positions_close, extent, gpu_forces, gpu_layout,
+                               shadow_check)
 
 pytestmark = pytest.mark.gpu
 
@@ -41,9 +43,9 @@ def _oracle(g, xy0, p, **kw):
 def test_one_batch_parity(name):
     g, xy0, cfg = build_config(name)
     p = _params(cfg, iters=1, max_batches=1)
-    got, _, _ = gpu_layout(g, xy0, **p)
-    ref, _, _ = _oracle(g, xy0, p)
-    assert_positions_close(got, ref, what=f"{name} one batch")
+    got, tr, _ = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, POS_TOL_BATCH, what=f"{name} one batch")
     # vertices outside the batch are untouched, bitwise
     b = min(cfg.batch, g.n)
     assert np.array_equal(got[b:], xy0[b:])
@@ -57,7 +59,7 @@ def test_one_iteration_parity(name):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"{name} one iteration")
-    assert abs(tr[0] - E[0]) <= 1e-3 * E[0], (tr[0], E[0])
+    assert_energy_close(tr[:1], E[:1], what=f"{name} one iteration")
 
 
 def test_C5_one_iteration_sampled_batches():
@@ -76,17 +78,37 @@ def test_C5_one_iteration_sampled_batches():
         ref = s_t[lo:hi].astype(np.float64) + f / np.hypot(f[:, 0], f[:, 1])[:, None]
         full_ref = s_t.astype(np.float64).copy()
         full_ref[lo:hi] = ref
-        ext = extent(full_ref)
-        err = np.abs(s_t1[lo:hi] - ref).max()
-        assert err <= 1e-4 * ext, (t, err, ext)
+        assert_positions_close(s_t1[lo:hi], ref, POS_TOL_BATCH, what=f"C5 batch {t} (shadowed)",
+                               ext=extent(full_ref))
+
+
+def _chain_lengths(n, deg, G):
+    """Longest fp32 summation chain behind one target's force in forces mode
+    (two-barrier phase R + phase U): repulsion -- one unit's
+    packed sweep of at most the CTA's whole chunk (ceil(ceil(n/G)/2) float4
+    steps), + 1 (pair lanes), + 31 (sub-range combine, <= BL_NSUB_MAX), +
+    ceil(G/32) + 5 (owner's lane-strided sum of the G partials + butterfly),
+    + 1 (f = S - C K^2 R); attraction -- <= 4 entries per lane per item, + 5
+    (butterfly), + ceil(items/32) + 5 (item sum), + 1."""
+    L_R = -(-(-(-n // G)) // 2) + 1 + 31 + -(-G // 32) + 5 + 1
+    items = -(-deg // 128)
+    L_A = 4 + 5 + -(-items // 32) + 5 + 1
+    return L_R, L_A
 
 
 @pytest.mark.parametrize("name", ["C2", "C4", "C5"])
 def test_forces_parity(name):
     """bl_forces (same device code) vs oracle f(i, c) for one batch of
-    targets.  Bound: 1e-4 x the sum of term magnitudes sum_j |term_ij| (fp32
-    accumulation of ~n/G-term chunks) + 1e-5 |f_i|."""
+    targets, against the worst-case fp32 error bound of the kernel's own
+    summation chains:
+        |df_i| <= u [(7 + L_R) C K^2 sum_{j != i} 1/d_ij
+                     + (12 + L_A) sum_{j in N(i)} (d_ij^2/K + C K^2/d_ij)] + 2u |f_i|,
+    u = 2^-24: each pair term carries <= 7u (Δ, d^2 by two FMAs, the paired
+    reciprocal), each neighbour term <= 12u (rsqrt.approx + the coefficient),
+    and a chain of length L adds <= L u of the sum of magnitudes it carries."""
+    import torch
     g, xy0, cfg = build_config(name)
+    G = torch.cuda.get_device_properties(0).multi_processor_count
     first = min(g.n - 1, 3 * cfg.batch) if name != "C5" else 0
     count = min(cfg.batch, g.n - first)
     got = gpu_forces(g, xy0, first, count)
@@ -99,9 +121,13 @@ def test_forces_parity(name):
         d = np.hypot(x[:, 0] - x[i, 0], x[:, 1] - x[i, 1])
         d[i] = np.inf
         nb = g.colidx[g.rowptr[i]:g.rowptr[i + 1]]
-        s = np.sum(1.0 / d) + np.sum(d[nb] ** 2) + 2 * np.sum(1.0 / d[nb])
-        bound[t] = 1e-4 * s + 1e-5 * np.hypot(*ref[t])
+        L_R, L_A = _chain_lengths(g.n, int(deg[i]), G)
+        s_r = cfg.C * cfg.K ** 2 * np.sum(1.0 / d)
+        s_a = np.sum(d[nb] ** 2 / cfg.K + cfg.C * cfg.K ** 2 / d[nb])
+        bound[t] = U32 * ((7 + L_R) * s_r + (12 + L_A) * s_a + 2 * np.hypot(*ref[t]))
     err = np.hypot(*(got - ref).T)
+    from tests.gpu_helpers import _log
+    _log(f"{name} forces", "force_err_over_bound", float((err / bound).max()), 1.0)
     bad = np.nonzero(err > bound)[0]
     assert bad.size == 0, (bad[:5], err[bad[:5]], bound[bad[:5]], deg[first + bad[:5]])
 
@@ -140,7 +166,7 @@ def test_batch_sizes_including_ragged_and_b_ge_n(b):
     got, tr, _ = gpu_layout(g, xy0, **p)
     ref, E, _ = _oracle(g, xy0, p)
     assert_positions_close(got, ref, what=f"b={b}")
-    np.testing.assert_allclose(tr, E, rtol=1e-3)
+    assert_energy_close(tr, E, what=f"b={b} one iteration")
     shadow_check(g, xy0, 4, _oracle, batch=b)
 
 
@@ -191,7 +217,7 @@ def test_coincident_vertex_pairs(stride):
         assert np.all(np.isfinite(got))
         assert_positions_close(got, ref, what=f"coincident stride {stride}")
         if "max_batches" not in p:
-            assert abs(tr[0] - E[0]) <= 1e-3 * E[0]
+            assert_energy_close(tr[:1], E[:1], what=f"coincident stride {stride}")
 
 
 def test_repulse_neighbors_flag():
@@ -209,7 +235,7 @@ def test_non_default_K_C_step_cooling():
     got, tr, _ = gpu_layout(g, xy0, **p)
     ref, E, _ = _oracle(g, xy0, p)
     assert_positions_close(got, ref, what="K,C,step")
-    np.testing.assert_allclose(tr, E, rtol=1e-3)
+    assert_energy_close(tr, E, what="K,C,step one iteration")
     shadow_check(g, xy0, 3, _oracle, batch=50, K=1.7, C=0.3, step0=0.25, cooling=0.9)
 
 
@@ -274,7 +300,7 @@ def test_full_run_energy_C1_protocol():
     """Full-run energy (north star: final energy within 1% relative).  The
     dynamics are chaotic: 1-ulp input perturbations move the
     oracle's own final energy by several %.  Protocol: (a) the first
-    iterations, before chaos sets in, match within 1e-3; (b) the GPU's final
+    iteration, before chaos sets in, matches within E_TOL; (b) the GPU's final
     energy lies within 3 standard deviations (+1%) of the ensemble of 12
     oracle runs from 1-ulp-perturbed inputs plus the fp32 oracle; (c) the
     relative difference to the unperturbed oracle and the ensemble spread
@@ -284,7 +310,7 @@ def test_full_run_energy_C1_protocol():
     _, tr, done = gpu_layout(g, xy0, **p)
     assert done == cfg.iters
     _, E, _ = _oracle(g, xy0, p)
-    np.testing.assert_allclose(tr[:2], E[:2], rtol=1e-3)
+    assert_energy_close(tr[:1], E[:1], what="C1 full run, iteration 0")
     finals = []
     rng = np.random.default_rng(0)
     up, down = np.float32(np.inf), np.float32(-np.inf)
@@ -318,7 +344,7 @@ def test_shadowing_C1(ckpt):
     got, tr, _ = gpu_layout(g, xt32, iters=1, batch=cfg.batch, step0=step_t)
     ref, E, _ = _oracle(g, xt32, dict(iters=1, batch=cfg.batch, step0=step_t))
     assert_positions_close(got, ref, what=f"shadow t={ckpt}")
-    assert abs(tr[0] - E[0]) <= 1e-4 * E[0]
+    assert_energy_close(tr[:1], E[:1], what=f"C1 shadow t={ckpt}")
 
 
 def test_invalid_params_rejected():
@@ -363,7 +389,7 @@ def test_pipelined_and_two_barrier_drivers_agree(name, monkeypatch):
     monkeypatch.setenv("BL_PIPELINE", "0")
     b, eb, _ = gpu_layout(g, xy0, **p)
     assert_positions_close(a, b, what="pipelined vs two-barrier")
-    np.testing.assert_allclose(ea, eb, rtol=1e-4)
+    assert_energy_close(ea, eb, tol=2e-6, what="pipelined vs two-barrier")
 
 
 def test_pipelined_max_batches_and_tol():
@@ -403,7 +429,7 @@ def test_C6_million_vertices_one_batch():
     f = oracle.forces(g.n, g.rowptr, g.colidx, xy0, 0, b)
     ref = xy0.astype(np.float64).copy()
     ref[:b] += f / np.hypot(f[:, 0], f[:, 1])[:, None]
-    assert_positions_close(got, ref, what="C6 one batch")
+    assert_positions_close(got, ref, POS_TOL_BATCH, what="C6 one batch")
     assert np.array_equal(got[b:], xy0[b:])
 
 
@@ -423,7 +449,7 @@ _FUZZ = [  # (graph, n-ish, batch, K, C, flags) -- both drivers, staged and L2 t
 def test_fuzz_shapes_one_iteration(case):
     """Random graph shapes x batch sizes that exercise both drivers (pipelined
     needs b even, <= 2048 and >= 4 batches), L2-resident targets and ragged
-    tails: one iteration vs the oracle, energy within 1e-3."""
+    tails: one iteration vs the oracle, energy within E_TOL."""
     from blgen import ba_graph
     kind, size, b, K, C, flags = case
     if kind == "rmat":
@@ -438,7 +464,7 @@ def test_fuzz_shapes_one_iteration(case):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"fuzz {case}")
-    assert abs(tr[0] - E[0]) <= 1e-3 * E[0]
+    assert_energy_close(tr[:1], E[:1], what=f"fuzz {case}")
 
 
 # ---- the asynchronous-phase driver (bl_run_async, the default for nb >= 4)
@@ -462,7 +488,7 @@ def test_drivers_one_iteration_vs_oracle(name, driver, monkeypatch):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"{name} one iteration ({driver[0]})")
-    np.testing.assert_allclose(tr[0], E[0], rtol=1e-4)
+    assert_energy_close(tr[:1], E[:1], what=f"{name} one iteration ({driver[0]})")
 
 
 @pytest.mark.parametrize("mb", [1, 2, 3, 4, 5, 43, 44, 45, 87])
@@ -595,6 +621,7 @@ def test_fuzz_shapes_async_forced(case, monkeypatch):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"fuzz async {case}")
+    assert_energy_close(tr[:1], E[:1], what=f"fuzz async {case}")
     again, tr2, _ = gpu_layout(g, xy0, **p)
     assert np.array_equal(got, again) and np.array_equal(tr, tr2)
 
@@ -614,3 +641,110 @@ def test_default_driver_per_config(name, expect):
         lay.layout_device(d, iters=1, batch=cfg.batch, max_batches=2)
         torch.cuda.synchronize()
         assert bl.bl_driver_name(lay.h) == expect
+
+
+def test_layout_then_forces_keeps_the_energy_of_the_layout():
+    """bl_energy reports the last LAYOUT call (bl.h): a bl_forces call in
+    between (another stream, forces mode) changes neither the iteration count
+    nor the trace (forces mode used to zero iters_done)."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0 = _small()
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=3, batch=16)
+        torch.cuda.synchronize()
+        e1, tr1, done1 = lay.energy(trace_len=3)
+        s2 = torch.cuda.Stream()
+        lay.forces(d, 0, 40, stream=s2)
+        lay.forces(d, 0, 40, stream=s2, algo=bl.BL_ALGO_BH)
+        torch.cuda.synchronize()
+        e2, tr2, done2 = lay.energy(trace_len=3)
+    assert done1 == done2 == 3 and e1 == e2 and np.array_equal(tr1, tr2)
+
+
+@pytest.mark.parametrize("driver", _DRIVERS + [("cluster", {})], ids=[d[0] for d in _DRIVERS] + ["cluster"])
+def test_max_batches_equal_to_all_batches(driver, monkeypatch):
+    """max_batches = iters x nb exactly: every driver reports what the oracle
+    reports (the stop is taken as a max_batches stop: iters - 1 completed
+    iterations) with the same final positions."""
+    _with_env(monkeypatch, driver[1])
+    g, xy0, cfg = build_config("C1" if driver[0] == "cluster" else "C3b256")
+    nb = -(-g.n // cfg.batch)
+    p = _params(cfg, iters=1, max_batches=nb)
+    got, _, done = gpu_layout(g, xy0, **p)
+    ref, _, rdone = _oracle(g, xy0, p)
+    assert done == rdone == 0
+    assert_positions_close(got, ref, what=f"max_batches = nb ({driver[0]})")
+
+
+def test_C5_one_iteration_free_running():
+    """The north star's "one full iteration ... <= 1e-4 x extent" at C5 itself
+    (SURVEY.md §8(c) acceptance 1): 256 dependent batches of 1,024 targets
+    against all 262,144 sources, free-running on both sides from the same
+    seeded bytes (Alg. 2), launched as bench.py launches it; plus
+    the iteration's energy."""
+    g, xy0, cfg = build_config("C5")
+    p = _params(cfg, iters=1)
+    got, tr, done = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert done == 1
+    assert_positions_close(got, ref, POS_TOL, what="C5 one iteration (free-running)")
+    assert_energy_close(tr[:1], E[:1], what="C5 one iteration (free-running)")
+
+
+def _golden_energy(name):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"energy_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (scripts/oracle_energy_golden.py {name})")
+    with open(path) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_run_energy_vs_oracle_golden(name):
+    """Full-run energy, the north star's "final energy within 1% relative"
+    (Energy: P:539), with the chaos protocol of SURVEY.md §8(c): the
+    oracle's traces (unperturbed fp64; 1-ulp-perturbed fp64 ensemble; fp32)
+    were written by scripts/oracle_energy_golden.py, which calls only
+    oracle/, from the same seeded bytes (checked by digest).
+      (i)   |E_gpu - E_oracle| / E_oracle at the final iteration <= 1% wherever
+            the oracle's own 1-ulp floor (ensemble spread) is below 1%;
+      (iii) the horizon: E_gpu(t) within 1% of E_oracle(t) for every t up to
+            the last iteration where the floor is <= 0.1%;
+      (iv)  E_gpu(final) inside [ensemble min - 1%, ensemble max + 1%]."""
+    import sys
+    sys.path.insert(0, __import__("os").path.join(__import__("os").path.dirname(__file__), "..",
+                                                  "scripts"))
+    from oracle_energy_golden import input_digest
+    gold = _golden_energy(name)
+    g, xy0, cfg = build_config(name)
+    assert gold["input_sha256"] == input_digest(g, xy0), "golden inputs differ from blgen's"
+    T = gold["iters"]
+    _, tr, done = gpu_layout(g, xy0, **_params(cfg, iters=T))
+    assert done == T
+    E = np.array(gold["oracle_f64"])
+    rel = np.abs(tr - E) / E
+    members = np.array(gold["ensemble_f64"]) if gold["ensemble_f64"] else E[None, :]
+    allrun = np.vstack([members, E[None, :]])
+    floor = (allrun.max(0) - allrun.min(0)) / E
+    from tests.gpu_helpers import _log
+    _log(f"{name} full run final", "energy_rel", rel[-1], 0.01)
+    _log(f"{name} full run final", "chaos_floor", floor[-1], 0.01)
+    print(f"{name} final energy (iteration {T}): gpu {tr[-1]:.9e} oracle {E[-1]:.9e} "
+          f"rel {rel[-1]:.3e}; 1-ulp floor {floor[-1]:.3e} ({len(members)} members)")
+    if not gold["ensemble_f64"]:
+        # unperturbed oracle only (C5: 72 min per oracle run on 6 host cores):
+        # the final-energy criterion alone
+        assert rel[-1] <= 0.01, rel[-1]
+        return
+    if floor[-1] < 0.01:
+        assert rel[-1] <= 0.01, (rel[-1], floor[-1])
+    h = np.nonzero(floor > 1e-3)[0]
+    horizon = int(h[0]) if h.size else T
+    assert np.all(rel[:horizon] <= 0.01), (horizon, rel[:horizon].max())
+    lo, hi = allrun[:, -1].min(), allrun[:, -1].max()
+    assert lo * 0.99 <= tr[-1] <= hi * 1.01, (tr[-1], lo, hi)
