@@ -321,7 +321,9 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     mufu_per_pair = 1 if args.r == -1.0 else 2   # r != -1: lg2 + ex2
     # SFU rate per SM per clock measured on this box (bl_microbench: MUFU.RCP
     # with clock64 on every SM), rounded to the lane count it resolves
-    mb_rates = [float(x) for x in bl.bl_microbench()]
+    mb = bl.bl_microbench()
+    mb_rates = [float(mb[k]) for k in ("ffma_per_clk_sm", "mufu_rcp_per_clk_sm",
+                                        "mufu_rsq_per_clk_sm", "ffma2_lane_ops_per_clk_sm")]
     mufu_clk = float(round(mb_rates[1])) if 8 <= mb_rates[1] <= 32 else float(MUFU_PER_CLK_SM)
     peak = nsm * mufu_clk * sm_max * 1e6 / mufu_per_pair
     achieved = pairs_per_step / t_step

@@ -55,7 +55,8 @@ def _load():
         vp = ctypes.c_void_p
         for sfx, R in (("f64", dbl), ("f32", flt)):
             f = getattr(lib, f"oracle_layout_{sfx}")
-            f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, dbl, dbl, i32, dbl, u32, vp, vp, ctypes.c_int]
+            f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, dbl, dbl, i32, dbl, u32, vp, vp, ctypes.c_int,
+                          ctypes.c_uint64]
             f.restype = ctypes.c_int
             f = getattr(lib, f"oracle_forces_{sfx}")
             f.argtypes = [i32, vp, vp, vp, i32, i32, R, R, u32, vp, ctypes.c_int]
@@ -64,6 +65,10 @@ def _load():
             f.argtypes = [vp, R, R, R, vp]
             f.restype = ctypes.c_int
         lib.oracle_max_threads.restype = ctypes.c_int
+        lib.oracle_permutation.argtypes = [i32, ctypes.c_uint64, i32, vp]
+        lib.oracle_permutation.restype = ctypes.c_int
+        lib.oracle_mix64.argtypes = [ctypes.c_uint64]
+        lib.oracle_mix64.restype = ctypes.c_uint64
         ll = ctypes.c_longlong
         lib.oracle_bh_forces.argtypes = [i32, vp, vp, vp, vp, i32, i32, dbl, dbl, dbl, vp, vp]
         lib.oracle_bh_forces.restype = ctypes.c_int
@@ -120,9 +125,10 @@ def max_threads() -> int:
 
 def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
            cooling=0.999, max_batches=0, tol=0.0, flags=0, threads=0, precision="f64",
-           a=2.0, r=-1.0):
+           a=2.0, r=-1.0, shuffle_seed=0):
     """Run Alg. 2 from xy0 ((n,2) any float dtype; converted to the oracle's
-    precision).  Returns (xy (n,2), energy[iters] fp64, iters_done)."""
+    precision).  shuffle_seed != 0: batch randomisation (readings R1-R2).
+    Returns (xy (n,2), energy[iters] fp64, iters_done)."""
     lib = _load()
     dt = np.float64 if precision == "f64" else np.float32
     xy = np.ascontiguousarray(np.asarray(xy0, dtype=dt).reshape(n, 2)).copy()
@@ -132,10 +138,25 @@ def layout(n, rowptr, colidx, xy0, *, iters, batch, K=1.0, C=1.0, step0=1.0,
     fn = getattr(lib, f"oracle_layout_{precision}")
     with _model(a, r):
         rc = fn(n, _ptr(rowptr), _ptr(colidx), _ptr(xy), iters, batch, K, C, step0, cooling,
-                max_batches, tol, flags, _ptr(energy), ctypes.byref(done), threads)
+                max_batches, tol, flags, _ptr(energy), ctypes.byref(done), threads,
+                int(shuffle_seed) & 0xFFFFFFFFFFFFFFFF)
     if rc != 0:
         raise ValueError("oracle_layout: invalid arguments")
     return xy, energy[:int(done.value) if tol > 0 else iters], int(done.value)
+
+
+def permutation(n, seed, it):
+    """pi_it of batch randomisation (readings R1-R2): int32 (n,)."""
+    lib = _load()
+    out = np.zeros(max(int(n), 1), np.int32)
+    if lib.oracle_permutation(int(n), int(seed) & 0xFFFFFFFFFFFFFFFF, int(it), _ptr(out)) != 0:
+        raise ValueError("oracle_permutation: invalid arguments")
+    return out[:int(n)]
+
+
+def mix64(z):
+    """The splitmix64 finaliser behind pi_it (for its known-answer pin)."""
+    return int(_load().oracle_mix64(int(z) & 0xFFFFFFFFFFFFFFFF))
 
 
 def forces(n, rowptr, colidx, xy, first=0, count=None, *, K=1.0, C=1.0, flags=0,

@@ -129,16 +129,23 @@ int SFX(oracle_forces)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
  * energy so far is written to energy[it]).  batch > n is clamped to n.
  * tol > 0: stop after the first iteration t >= 1 with |E_t - E_{t-1}| < tol
  * (the convergence criterion of §4.5).
+ * shuffle_seed != 0: batch randomisation (§4.3.3, readings R1-R2 in
+ * bl_oracle.c): batch t of iteration it is pi_it(t b .. ); 0 = sequential.
  * Returns 0, or -1 on invalid arguments. */
 int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
                        REAL *xy, int32_t iters, int32_t batch, REAL K, REAL C,
                        double step0, double cooling, int32_t max_batches,
                        double tol, uint32_t flags, double *energy,
-                       int32_t *iters_done, int threads) {
+                       int32_t *iters_done, int threads, uint64_t shuffle_seed) {
   if (n < 1 || iters < 0 || batch < 1) return -1;
   if (batch > n) batch = n;
   REAL *ct = (REAL *)malloc(sizeof(REAL) * 2 * (size_t)batch);
-  if (!ct) return -1;
+  int32_t *vid = (int32_t *)malloc(sizeof(int32_t) * (size_t)batch);
+  if (!ct || !vid) {
+    free(ct);
+    free(vid);
+    return -1;
+  }
   double step = step0;
   int32_t batches_done = 0;
   int32_t it_done = 0;
@@ -152,6 +159,9 @@ int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
     const REAL stepr = (REAL)step;
     for (int32_t lo = 0; lo < n; lo += batch) {
       const int32_t hi = (lo + batch < n) ? lo + batch : n;
+      /* the batch's vertices: lo..hi-1, or pi_it(lo..hi-1) with batch
+       * randomisation (readings R1-R2; pi = identity for seed 0) */
+      for (int32_t k = lo; k < hi; ++k) vid[k - lo] = oracle_perm(shuffle_seed, it, n, k);
       /* forces of the whole batch against frozen coordinates */
 #ifdef _OPENMP
 #pragma omp parallel
@@ -161,15 +171,16 @@ int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
 #ifdef _OPENMP
 #pragma omp for schedule(static)
 #endif
-        for (int32_t i = lo; i < hi; ++i) {
-          SFX(force_of)(n, rowptr, colidx, xy, i, K, C, flags, mark,
-                        &ct[2 * (i - lo)], &ct[2 * (i - lo) + 1]);
+        for (int32_t k = lo; k < hi; ++k) {
+          SFX(force_of)(n, rowptr, colidx, xy, vid[k - lo], K, C, flags, mark,
+                        &ct[2 * (k - lo)], &ct[2 * (k - lo) + 1]);
         }
         free(mark);
       }
       /* then the batch update, in order */
-      for (int32_t i = lo; i < hi; ++i) {
-        E = E + SFX(apply_update)(&xy[2 * i], ct[2 * (i - lo)], ct[2 * (i - lo) + 1], stepr);
+      for (int32_t k = lo; k < hi; ++k) {
+        E = E + SFX(apply_update)(&xy[2 * vid[k - lo]], ct[2 * (k - lo)], ct[2 * (k - lo) + 1],
+                                  stepr);
       }
       ++batches_done;
       if (max_batches > 0 && batches_done >= max_batches) {
@@ -187,6 +198,7 @@ int SFX(oracle_layout)(int32_t n, const int32_t *rowptr, const int32_t *colidx,
     }
   }
   free(ct);
+  free(vid);
   if (iters_done) *iters_done = it_done;
   (void)threads;
   return 0;

@@ -376,7 +376,11 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     size_t cap = 0;
     if ((s = grow(h, h->d_e_cta, cap, (size_t)2 * G)) != BL_OK) return s;
   }
-  if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
+  // the energy trace belongs to the last layout call (bl_energy): forces mode
+  // neither writes nor reallocates it
+  if (!forces_mode &&
+      (s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK)
+    return s;
 
   BLKParams k{};
   k.n = n;
@@ -520,7 +524,9 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
     size_t cap = 0;
     if ((s = grow(h, h->d_e_cta, cap, (size_t)2 * G)) != BL_OK) return s;
   }
-  if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
+  if (!forces_mode &&
+      (s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK)
+    return s;
   BHKParams k{};
   k.n = n;
   k.b = b;

@@ -65,17 +65,20 @@ def alg1(n, A, c0, iters, K=1.0, R=1.0, step0=1.0, factor=0.999):
 
 
 def alg2(n, A, c0, iters, BS, K=1.0, R=1.0, step0=1.0, factor=0.999,
-         repulse_neighbors=False, a=2.0, r=-1.0):
+         repulse_neighbors=False, a=2.0, r=-1.0, perms=None):
     """Algorithm 2 semantics: consecutive minibatches, forces of
-    a batch against frozen coordinates, then the batch update."""
+    a batch against frozen coordinates, then the batch update.  perms: one
+    vertex order per iteration (batch randomisation, §4.3.3):
+    batch t is perms[it][t BS : (t+1) BS]; None = the sequential order."""
     c = [[float(p[0]), float(p[1])] for p in c0]
     step = step0
     energies = []
     BS = min(BS, n)
-    for _ in range(iters):
+    for it in range(iters):
         energy = 0.0
+        order = list(range(n)) if perms is None else [int(v) for v in perms[it]]
         for lo in range(0, n, BS):
-            batch = range(lo, min(lo + BS, n))
+            batch = order[lo:min(lo + BS, n)]
             ct = [_force(n, A, c, i, K, R, repulse_neighbors, a, r) for i in batch]
             for i, (fx, fy) in zip(batch, ct):
                 norm = math.hypot(fx, fy)

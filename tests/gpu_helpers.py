@@ -32,6 +32,30 @@ def _log(what, kind, value, gate):
                                  "gate": float(gate)}) + "\n")
 
 
+def energy_gate(g, state, params, oracle_layout=None):
+    """Energy gate of ONE iteration from `state`: E_TOL, or
+    twice the fp32 arithmetic floor of that very iteration when larger --
+    |E_f32 - E_f64| / E_f64 of the oracle run in fp32 (sequential sums,
+    longer chains than the kernel's) -- because inside an iteration every
+    batch sees the rounding of the batches before it, amplified by close
+    encounters (1/d^2 force gradients); with many dependent batches (b = 1 on
+    a small graph) that floor reaches 1e-4.  Skipped above 20,000 vertices
+    (the large configs' floors are < 3e-7)."""
+    import oracle
+    if g.n > 20000:
+        return E_TOL
+    q = dict(params)
+    kw = dict(iters=1, batch=q["batch"], K=q.get("K", 1.0), C=q.get("C", 1.0),
+              step0=q.get("step0", 1.0), cooling=q.get("cooling", 0.999),
+              flags=q.get("flags", 0), a=q.get("a", 2.0), r=q.get("r", -1.0),
+              shuffle_seed=q.get("shuffle_seed", 0))
+    _, e64, _ = oracle.layout(g.n, g.rowptr, g.colidx, state, **kw)
+    _, e32, _ = oracle.layout(g.n, g.rowptr, g.colidx, state, precision="f32", **kw)
+    floor = abs(e32[0] - e64[0]) / e64[0] if e64[0] > 0 else 0.0
+    _log("fp32 floor of the iteration", "energy_fp32_floor", floor, E_TOL)
+    return max(E_TOL, 2.0 * floor)
+
+
 def assert_energy_close(got, ref, tol=E_TOL, what=""):
     """|E_gpu - E_oracle| <= tol x E_oracle for every entry (E = 0 exactly
     when every force is 0, compared exactly)."""
@@ -112,7 +136,8 @@ def shadow_check(g, xy0, iters, oracle_layout, tol=POS_TOL, **params):
         got, tr, _ = gpu_layout(g, state, **p)
         ref, E, _ = oracle_layout(g, state, p)
         worst = max(worst, assert_positions_close(got, ref, tol, what=f"shadowed iteration {t}"))
-        assert_energy_close(tr[:1], E[:1], what=f"shadowed iteration {t}")
+        assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, state, p),
+                            what=f"shadowed iteration {t}")
         state = got
         step = step * cooling
     return worst

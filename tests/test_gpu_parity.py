@@ -14,7 +14,7 @@ import pytest
 import oracle
 from blgen import (build_config, cycle_graph, edges_to_csr, grid_graph, rmat_graph, star_graph,
                    uniform_coords)
-from tests.gpu_helpers import (POS_TOL, POS_TOL_BATCH, U32, assert_energy_close,
+from tests.gpu_helpers import (POS_TOL, POS_TOL_BATCH, U32, assert_energy_close, energy_gate,
                                assert_positions_close, extent, gpu_forces, gpu_layout,
                                shadow_check)
 
@@ -59,7 +59,7 @@ def test_one_iteration_parity(name):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"{name} one iteration")
-    assert_energy_close(tr[:1], E[:1], what=f"{name} one iteration")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p), what=f"{name} one iteration")
 
 
 def test_C5_one_iteration_sampled_batches():
@@ -166,7 +166,7 @@ def test_batch_sizes_including_ragged_and_b_ge_n(b):
     got, tr, _ = gpu_layout(g, xy0, **p)
     ref, E, _ = _oracle(g, xy0, p)
     assert_positions_close(got, ref, what=f"b={b}")
-    assert_energy_close(tr, E, what=f"b={b} one iteration")
+    assert_energy_close(tr, E, tol=energy_gate(g, xy0, p), what=f"b={b} one iteration")
     shadow_check(g, xy0, 4, _oracle, batch=b)
 
 
@@ -235,7 +235,7 @@ def test_non_default_K_C_step_cooling():
     got, tr, _ = gpu_layout(g, xy0, **p)
     ref, E, _ = _oracle(g, xy0, p)
     assert_positions_close(got, ref, what="K,C,step")
-    assert_energy_close(tr, E, what="K,C,step one iteration")
+    assert_energy_close(tr, E, tol=energy_gate(g, xy0, p), what="K,C,step one iteration")
     shadow_check(g, xy0, 3, _oracle, batch=50, K=1.7, C=0.3, step0=0.25, cooling=0.9)
 
 
@@ -344,7 +344,8 @@ def test_shadowing_C1(ckpt):
     got, tr, _ = gpu_layout(g, xt32, iters=1, batch=cfg.batch, step0=step_t)
     ref, E, _ = _oracle(g, xt32, dict(iters=1, batch=cfg.batch, step0=step_t))
     assert_positions_close(got, ref, what=f"shadow t={ckpt}")
-    assert_energy_close(tr[:1], E[:1], what=f"C1 shadow t={ckpt}")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xt32, dict(batch=cfg.batch, step0=step_t)),
+                        what=f"C1 shadow t={ckpt}")
 
 
 def test_invalid_params_rejected():
@@ -464,7 +465,7 @@ def test_fuzz_shapes_one_iteration(case):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"fuzz {case}")
-    assert_energy_close(tr[:1], E[:1], what=f"fuzz {case}")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p), what=f"fuzz {case}")
 
 
 # ---- the asynchronous-phase driver (bl_run_async, the default for nb >= 4)
@@ -488,7 +489,8 @@ def test_drivers_one_iteration_vs_oracle(name, driver, monkeypatch):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"{name} one iteration ({driver[0]})")
-    assert_energy_close(tr[:1], E[:1], what=f"{name} one iteration ({driver[0]})")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p),
+                        what=f"{name} one iteration ({driver[0]})")
 
 
 @pytest.mark.parametrize("mb", [1, 2, 3, 4, 5, 43, 44, 45, 87])
@@ -621,7 +623,7 @@ def test_fuzz_shapes_async_forced(case, monkeypatch):
     ref, E, _ = _oracle(g, xy0, p)
     assert done == 1
     assert_positions_close(got, ref, what=f"fuzz async {case}")
-    assert_energy_close(tr[:1], E[:1], what=f"fuzz async {case}")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p), what=f"fuzz async {case}")
     again, tr2, _ = gpu_layout(g, xy0, **p)
     assert np.array_equal(got, again) and np.array_equal(tr, tr2)
 
