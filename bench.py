@@ -371,6 +371,8 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     if not args.no_bh:
         line["bh"] = bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, t_step)
     line["attraction"] = bench_attraction(lay, d_xy0, params, stream, flush, g, peaks)
+    if not args.no_shuffle and cfg.batch <= 2048:
+        line["shuffle"] = bench_shuffle(args, lay, d_xy0, params, stream, flush, cfg, t_step)
     if args.latency_configs and args.r == -1.0:
         line["latency"] = bench_latency(args, dev, stream, flush, peak)
     lay.close()
@@ -459,6 +461,47 @@ def bench_latency(args, dev, stream, flush, peak_per_sm_clk):
     return out
 
 
+def _time_layout(lay, d_xy0, params, stream, flush, steps, warmup=2):
+    import torch
+    d = torch.empty_like(d_xy0)
+    for _ in range(warmup):
+        d.copy_(d_xy0)
+        lay.layout_device(d, stream=stream, **params)
+    torch.cuda.synchronize()
+    ms = []
+    for i in range(steps):
+        d.copy_(d_xy0)
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        lay.layout_device(d, stream=stream, **params)
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    return float(np.median(ms)) / 1e3
+
+
+def bench_shuffle(args, lay, d_xy0, params, stream, flush, cfg, t_default):
+    """Secondary object: batch randomisation (shuffle_seed, §4.3.3)
+    on the same workload -- it runs on the two-barrier driver, so the cost is
+    split into the driver (sequential batches on the two-barrier driver) and
+    the reshuffle itself ("Randomization also introduces overhead")."""
+    import paper_2002_08233_b200 as bl
+    steps = max(2, min(args.steps, 3))
+    t_shuf = _time_layout(lay, d_xy0, dict(params, shuffle_seed=1), stream, flush, steps)
+    drv = bl.bl_driver_name(lay.h)
+    os.environ["BL_PIPELINE"] = "0"
+    try:
+        t_seq2 = _time_layout(lay, d_xy0, params, stream, flush, steps)
+    finally:
+        os.environ.pop("BL_PIPELINE", None)
+    return {"shuffle_seed": 1, "driver": drv, "iters_per_sec": cfg.iters / t_shuf,
+            "ms_per_step": 1e3 * t_shuf,
+            "sequential_same_driver_iters_per_sec": cfg.iters / t_seq2,
+            "default_iters_per_sec": cfg.iters / t_default,
+            "cost_vs_default": t_shuf / t_default, "cost_of_reshuffle_alone": t_shuf / t_seq2}
+
+
 def bench_attraction(lay, d_xy0, params, stream, flush, g, peaks):
     """Step a5 alone (bl_forces with BL_ATTRACTION_ONLY over all n vertices:
     the CSR attraction + neighbour correction of one whole iteration, edge-
@@ -537,6 +580,7 @@ def main(argv=None):
     ap.add_argument("--backend", default="nccl")
     ap.add_argument("--prof", action="store_true", help="add a phase profile (extra untimed run)")
     ap.add_argument("--no-bh", action="store_true", help="skip the secondary BatchLayoutBH line")
+    ap.add_argument("--no-shuffle", action="store_true", help="skip the batch-randomisation object")
     ap.add_argument("--theta", type=float, default=1.2, help="BatchLayoutBH MAC threshold (P:869)")
     ap.add_argument("--latency-configs", default="C2,C3b256,C4",
                     help="secondary latency-bound configs ('' to skip)")

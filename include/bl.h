@@ -85,12 +85,20 @@ typedef struct {
   float r;             /* the repulsive force magnitude is C K^2 d^r, r in
                           [-3, 1); -1 = the paper's (Fruchterman-Reingold).
                           r != -1 costs two SFU ops per pair instead of one    */
+  uint64_t shuffle_seed; /* batch randomisation (§4.3.3, Fig. S3;
+                          readings R1-R2 in DESIGN.md §3): 0 = the paper's
+                          default sequential batches; otherwise iteration it
+                          walks the batches of a fresh seeded permutation
+                          pi_it of the vertex ids (batch t = pi_it(t b ..)),
+                          a keyed Feistel bijection any implementation can
+                          evaluate.  BL_ALGO_EXACT only (BL_EINVAL with BH);
+                          runs on the two-barrier driver     */
 } bl_params;
 
 /* Fill p with the paper's defaults: iters 600 (the CLI default),
  * batch 256, K = 1, C = 1, step0 = 1.0, cooling = 0.999, tol = 0,
  * max_batches = 0, flags = 0, algo = BL_ALGO_EXACT, theta = 1.2,
- * a = 2, r = -1. */
+ * a = 2, r = -1, shuffle_seed = 0 (sequential batches). */
 void bl_params_default(bl_params *p);
 
 /* Create a context on the current CUDA device for the undirected graph G

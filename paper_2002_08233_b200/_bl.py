@@ -34,6 +34,7 @@ class bl_params(ctypes.Structure):
         ("theta", ctypes.c_float),
         ("a", ctypes.c_float),
         ("r", ctypes.c_float),
+        ("shuffle_seed", ctypes.c_uint64),
     ]
 
 

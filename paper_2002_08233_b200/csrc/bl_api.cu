@@ -60,6 +60,7 @@ extern "C" void bl_params_default(bl_params *p) {
   p->theta = 1.2f;
   p->a = 2.0f;
   p->r = -1.0f;
+  p->shuffle_seed = 0;
 }
 
 // (a, r)-energy model codes shared by both kernels (reading C15)
@@ -334,6 +335,10 @@ static bl_status check_params(bl_ctx *h, const bl_params *p) {
     return bl_fail(h, BL_EINVAL, "theta must be >= 0");
   if (!(p->a >= 0.f && p->a <= 4.f)) return bl_fail(h, BL_EINVAL, "a must be in [0, 4]");
   if (!(p->r >= -3.f && p->r < 1.f)) return bl_fail(h, BL_EINVAL, "r must be in [-3, 1)");
+  if (p->shuffle_seed && p->algo != BL_ALGO_EXACT)
+    return bl_fail(h, BL_EINVAL, "shuffle_seed (batch randomisation) needs BL_ALGO_EXACT");
+  if (p->shuffle_seed && h && std::min(p->batch, h->n) > BL_TGT_CAP)
+    return bl_fail(h, BL_EINVAL, "shuffle_seed needs batch <= %d", BL_TGT_CAP);
   return BL_OK;
 }
 
@@ -410,7 +415,12 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // one barrier per batch needs >= 4 batches per iteration,
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
-  k.pipelined = !forces_mode && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
+  // batch randomisation (readings R1-R2): the two-barrier driver (its phase U
+  // takes batch positions, not owned vertices)
+  k.shuf_seed = forces_mode ? 0ull : (unsigned long long)p->shuffle_seed;
+  k.shuf_h = 1;
+  while ((1LL << (2 * k.shuf_h)) < (long long)n) ++k.shuf_h;
+  k.pipelined = !forces_mode && k.shuf_seed == 0 && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
                 (b + G - 1) / G <= BL_ETASK_MAX &&
                 red_cap_for(chunk4_for(n, G)) / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
                 env_int("BL_PIPELINE", 1) != 0;
@@ -607,6 +617,7 @@ static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
   *used = false;
   const int n = h->n, b = std::min(p->batch, n);
   if (env_int("BL_CLUSTER", 1) == 0) return BL_OK;
+  if (p->shuffle_seed) return BL_OK;  // randomised batches: whole-GPU two-barrier driver
   const long long pairs_max = env_int("BL_CLUSTER_PAIRS", 1000000);
   if ((long long)b * n > pairs_max) return BL_OK;
   int dev = 0, optin = 0;

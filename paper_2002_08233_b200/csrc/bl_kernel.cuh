@@ -113,6 +113,10 @@ struct BLKParams {
   int amode, rmode;
   float a_half, r_half;  // (a-1)/2, (r-1)/2: vector coefficients d^(a-1), d^(r-1)
   int forces_mode, first, count;
+  // batch randomisation (readings R1-R2): 0 = sequential; else
+  // iteration it walks the batches of pi_it (two-barrier driver only)
+  unsigned long long shuf_seed;
+  int shuf_h;            // Feistel half width: 2^(2h) >= n
   int attr_only;         // forces_mode + BL_ATTRACTION_ONLY: a5 alone (no sweep, R = 0)
   float2 *xy;
   const int *rowptr, *colidx;
@@ -156,6 +160,52 @@ __device__ __forceinline__ float bl_rsqrt(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// ---- batch randomisation (§4.3.3; readings R1-R2 of DESIGN.md §3):
+// pi_it is a 4-round Feistel bijection of [0, 2^(2h)) keyed from splitmix64,
+// restricted to [0, n) by cycle walking -- integer arithmetic only, so any
+// thread evaluates pi_it(x) for its own x, no permutation array.
+__host__ __device__ __forceinline__ unsigned long long bl_mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+struct BLPerm {
+  const unsigned long long *key;  // 4 round keys of pi_it, in shared memory
+  int h, n, on;
+};
+// round keys of pi_it into key[4] (shared; every thread computes the same
+// values, so no barrier is needed before use by the writing threads' CTA
+// beyond the one at the caller)
+__device__ __forceinline__ BLPerm bl_perm_make(unsigned long long seed, int h, int n, int it,
+                                               unsigned long long *key) {
+  BLPerm P;
+  P.on = seed != 0ull;
+  P.h = h;
+  P.n = n;
+  P.key = key;
+  if (P.on && threadIdx.x < 4)
+    key[threadIdx.x] =
+        bl_mix64(seed ^ bl_mix64((unsigned long long)it * 4ull + (unsigned long long)threadIdx.x));
+  return P;
+}
+__device__ __forceinline__ int bl_perm(const BLPerm &P, int x) {
+  if (!P.on) return x;
+  const unsigned long long mask = (1ull << P.h) - 1ull;
+  unsigned long long y = (unsigned long long)x;
+  do {
+    unsigned long long L = y >> P.h, R = y & mask;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const unsigned long long t = L ^ (bl_mix64(P.key[r] ^ R) >> (64 - P.h));
+      L = R;
+      R = t;
+    }
+    y = (L << P.h) | R;
+  } while (y >= (unsigned long long)P.n);
+  return (int)y;
+}
+
 // ---- packed fp32x2 (sm_100a FADD2/FFMA2/FMUL2): two pair evaluations per
 // issue slot.  Operand (a, b) lives in one 64-bit register pair.
 typedef unsigned long long bl_f2;
@@ -455,19 +505,105 @@ __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int b
 }
 
 // ---------------------------------------------------------------- phase R
+// Attraction items of a RANDOMISED batch (readings R1-R2): batch position k
+// holds vertex pi(lo + k), whose items are item_ptr[v] .. item_ptr[v+1]; the
+// batch's items are numbered through ioff[k] = sum_{k' < k} items(pi(lo+k'))
+// (a block-wide scan, identical in every CTA), so all warps of the grid
+// share them as in the sequential case.  Requires bt <= BL_TGT_CAP.
+__device__ __forceinline__ void bl_batch_item_offsets(const BLKParams &p, const BLPerm &P, int lo,
+                                                      int bt, int *ioff) {
+  // per-thread contiguous chunks, then a scan of the chunk totals
+  const int per = (bt + BL_NT - 1) / BL_NT;
+  const int a = threadIdx.x * per, e = min(a + per, bt);
+  int tot = 0;
+  for (int k = a; k < e; ++k) {
+    const int v = bl_perm(P, lo + k);
+    const int m = __ldg(p.item_ptr + v + 1) - __ldg(p.item_ptr + v);
+    ioff[k + 1] = m;
+    tot += m;
+  }
+  // inclusive scan of the per-thread totals (warp shuffles + warp totals)
+  __shared__ int wsum[BL_NW_MAX];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  int run = base + x - tot;  // exclusive prefix of this thread's chunk
+  if (threadIdx.x == 0) ioff[0] = 0;
+  for (int k = a; k < e; ++k) {
+    run += ioff[k + 1];
+    ioff[k + 1] = run;
+  }
+  __syncthreads();
+}
+
 template <int T, int TP>
 __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, const float4 *src4,
-                                           float2 *tgt, float2 *red, int *unit_ctr, BLProf &pf) {
+                                           float2 *tgt, float2 *red, int *unit_ctr, BLProf &pf,
+                                           const BLPerm &P, int *ioff) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tgt_smem = bt <= BL_TGT_CAP;
 
   // (0) stage the batch's targets (frozen coordinates)
   if (tgt_smem && !p.attr_only)
-    for (int i = threadIdx.x; i < bt; i += BL_NT) tgt[i] = __ldcg(p.xy + lo + i);
+    for (int i = threadIdx.x; i < bt; i += BL_NT) tgt[i] = __ldcg(p.xy + bl_perm(P, lo + i));
+
+  // (1r) randomised batch: items through pi and the batch item offsets
+  if (P.on) {
+    bl_batch_item_offsets(p, P, lo, bt, ioff);
+    const int GW = G * BL_NW, ni = ioff[bt];
+    const float rep = (p.flags & 1u) ? 0.f : p.ck2;
+    for (int it = c * BL_NW + warp; it < ni; it += GW) {
+      int l = 0, h = bt;  // the position k with ioff[k] <= it < ioff[k+1]
+      while (h - l > 1) {
+        const int m = (l + h) >> 1;
+        if (ioff[m] <= it) l = m;
+        else h = m;
+      }
+      const int v = bl_perm(P, lo + l);
+      const int ag = __ldg(p.item_ptr + v) + (it - ioff[l]);
+      const int k0 = __ldg(p.item_k0 + ag), k1 = __ldg(p.item_k0 + ag + 1);
+      const float2 ci = __ldcg(p.xy + v);
+      float sx = 0.f, sy = 0.f;
+      int jj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + lane + 32 * u;
+        jj[u] = k < k1 ? __ldg(p.colidx + k) : -1;
+      }
+      float2 cj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cj[u] = jj[u] >= 0 ? __ldcg(p.xy + jj[u]) : ci;
+      auto scan_row = [&](auto fast) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (jj[u] < 0) continue;
+          const float dx = cj[u].x - ci.x, dy = cj[u].y - ci.y;
+          const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+          const float rs = bl_rsqrt(d2);
+          const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+          sx = fmaf(coef, dx, sx);
+          sy = fmaf(coef, dy, sy);
+        }
+      };
+      if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});
+      else scan_row(std::false_type{});
+      sx = bl_warp_sum0(sx);
+      sy = bl_warp_sum0(sy);
+      if (lane == 0) p.attr[it] = make_float2(sx, sy);
+    }
+  }
 
   // (1) attraction items of this batch, spread over all warps of the grid
-  {
+  if (!P.on) {
     const int ib = __ldg(p.item_ptr + lo), ie = __ldg(p.item_ptr + lo + bt);
     const int GW = G * BL_NW;
     // the next item's (v, k0, k1) is loaded while the current one is
@@ -533,15 +669,24 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
 // w-th, (w+NW)-th, ... of them.  All loads of one vertex are issued before
 // any is consumed (one L2 round trip for the partials + item bounds, one for
 // the attraction items).  Accumulates ||f||^2 into e_acc (lane 0).
+// Randomised batches (P.on): CTA c takes the batch POSITIONS k = c (mod G),
+// vertex pi(lo + k), reading its old coordinate from xy (not the owner's
+// resident copy, which another CTA holds) and its attraction items through
+// ioff; the owners refresh their resident copies after the next grid
+// barrier (bl_refresh_resident).
 __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, double stepd,
-                                           float4 *src4, double &e_acc) {
+                                           float4 *src4, double &e_acc, const BLPerm &P,
+                                           const int *ioff) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int v0 = lo + ((c - lo % G) + G) % G;
+  const int v0 = P.on ? c : lo + ((c - lo % G) + G) % G;
+  const int vend = P.on ? bt : lo + bt;
   const int ib = __ldg(p.item_ptr + lo);
-  for (int v = v0 + warp * G; v < lo + bt; v += BL_NW * G) {
-    const int local = v - lo;
-    const int a0 = __ldg(p.item_ptr + v) - ib, a1 = __ldg(p.item_ptr + v + 1) - ib;
+  for (int w = v0 + warp * G; w < vend; w += BL_NW * G) {
+    const int local = P.on ? w : w - lo;
+    const int v = P.on ? bl_perm(P, lo + w) : w;
+    const int a0 = P.on ? ioff[w] : __ldg(p.item_ptr + v) - ib;
+    const int a1 = P.on ? ioff[w + 1] : __ldg(p.item_ptr + v + 1) - ib;
     const float2 *row = p.part + (size_t)local * G;
     float rx = 0.f, ry = 0.f;
     if (!p.attr_only) {
@@ -571,16 +716,31 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
         const double q = (double)fx * fx + (double)fy * fy;
         if (q > 0.0) {
           const double s = stepd / sqrt(q);
-          float2 cv = bl_src_get(src4, (v - c) / G);  // the owner's resident copy of xy[v]
+          // the owner's resident copy of xy[v] (randomised: xy itself, frozen
+          // until this store -- no other warp reads xy[v] in this phase)
+          float2 cv = P.on ? __ldcg(p.xy + v) : bl_src_get(src4, (v - c) / G);
           cv.x = (float)((double)cv.x + s * fx);
           cv.y = (float)((double)cv.y + s * fy);
           p.xy[v] = cv;
-          bl_src_set(src4, (v - c) / G, cv);
+          if (!P.on) bl_src_set(src4, (v - c) / G, cv);
         }
         e_acc += q;
       }
     }
   }
+}
+
+// After the grid barrier that follows a randomised batch's phase U: every
+// CTA copies the new coordinates of the batch members it owns (v = c mod G)
+// from xy into its resident source chunk.
+__device__ __forceinline__ void bl_refresh_resident(const BLKParams &p, const BLPerm &P, int lo,
+                                                    int bt, float4 *src4) {
+  const int G = gridDim.x, c = blockIdx.x;
+  for (int k = threadIdx.x; k < bt; k += BL_NT) {
+    const int v = bl_perm(P, lo + k);
+    if (v % G == c) bl_src_set(src4, (v - c) / G, __ldcg(p.xy + v));
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------- pipelined driver (nb >= 4)
@@ -627,6 +787,8 @@ struct BLShared {
   double e_acc;   // this CTA's energy of the running iteration
   double e_task[BL_ETASK_MAX];
   double e_warp[BL_NW_MAX];
+  int ioff[BL_TGT_CAP + 1];  // randomised batches: item offsets per position
+  unsigned long long pkey[4];  // randomised batches: round keys of pi_it
   // CSR rows (<= 32 entries) of this CTA's owned vertices of a batch, staged
   // by the control task of the phase that sweeps the batch, used by the
   // update tasks one phase later (two fewer dependent L2 round trips on the
@@ -1401,7 +1563,8 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
 
   if (p.forces_mode) {
     double e_dummy = 0.0;
-    bl_phase_R<T, TP>(p, p.first, p.count, src4, tgt, red, unit_ctr, pf);
+    const BLPerm P0 = bl_perm_make(0ull, 1, p.n, 0, sh.pkey);  // identity
+    bl_phase_R<T, TP>(p, p.first, p.count, src4, tgt, red, unit_ctr, pf, P0, sh.ioff);
     bl_grid_sync(p.bar, bar_target, unit_ctr);
     if (p.attr_only) {
       // a5 alone over a range of any size: one thread per vertex sums its
@@ -1419,7 +1582,7 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
       }
       return;
     }
-    bl_phase_U(p, p.first, p.count, 0.0, src4, e_dummy);
+    bl_phase_U(p, p.first, p.count, 0.0, src4, e_dummy, P0, sh.ioff);
     return;
   }
 
@@ -1440,13 +1603,16 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
   bool stop = false;
   for (; it < p.iters && !stop; ++it) {
     e_acc = 0.0;
+    __syncthreads();  // every thread is past the previous iteration's uses of pkey
+    const BLPerm P = bl_perm_make(p.shuf_seed, p.shuf_h, p.n, it, sh.pkey);  // pi_it (R1)
+    __syncthreads();
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b;
       const int bt = min(p.b, p.n - lo);
-      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, unit_ctr, pf);
+      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, unit_ctr, pf, P, sh.ioff);
       bl_grid_sync(p.bar, bar_target, unit_ctr);
       pf.mark(3);
-      bl_phase_U(p, lo, bt, step, src4, e_acc);
+      bl_phase_U(p, lo, bt, step, src4, e_acc, P, sh.ioff);
       pf.mark(4);
       ++batches;
       const bool last = (t == p.nb - 1);
@@ -1461,6 +1627,7 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
         }
       }
       bl_grid_sync(p.bar, bar_target, unit_ctr);
+      if (P.on) bl_refresh_resident(p, P, lo, bt, src4);
       pf.mark(5);
       if (last || stop) {
         // every CTA reduces the per-CTA energies in the same order, so the

@@ -1,0 +1,119 @@
+"""Batch randomisation on the GPU (shuffle_seed, §4.3.3; readings
+R1-R2 of DESIGN.md §3) vs the oracle's, through the C-ABI.  Marked gpu.
+
+Both sides evaluate the same keyed Feistel permutation pi_it with integer
+arithmetic (no shared code: oracle/bl_oracle.c vs csrc/bl_kernel.cuh)."""
+import numpy as np
+import pytest
+
+import oracle
+from blgen import build_config, grid_graph, uniform_coords
+from tests.gpu_helpers import (POS_TOL, POS_TOL_BATCH, assert_energy_close,
+                               assert_positions_close, energy_gate, gpu_layout)
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["C1", "C2", "C3b64", "C3b256", "C3b1024", "C4", "C5"]
+SEED = 20022
+
+
+def _params(cfg, **kw):
+    d = dict(iters=cfg.iters, batch=cfg.batch, K=cfg.K, C=cfg.C, step0=cfg.step0,
+             cooling=cfg.cooling, shuffle_seed=SEED)
+    d.update(kw)
+    return d
+
+
+def _oracle(g, xy0, p):
+    return oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=p["iters"], batch=p["batch"],
+                         K=p["K"], C=p["C"], step0=p["step0"], cooling=p["cooling"],
+                         max_batches=p.get("max_batches", 0), flags=p.get("flags", 0),
+                         shuffle_seed=p["shuffle_seed"])
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_shuffled_one_batch_parity(name):
+    """One randomised batch (pi_0(0 .. b-1)): positions vs the oracle, and
+    exactly the batch's members may move."""
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=1, max_batches=1)
+    got, _, _ = gpu_layout(g, xy0, **p)
+    ref, _, _ = _oracle(g, xy0, p)
+    assert_positions_close(got, ref, POS_TOL_BATCH, what=f"{name} shuffled one batch")
+    b = min(cfg.batch, g.n)
+    others = np.setdiff1d(np.arange(g.n), oracle.permutation(g.n, SEED, 0)[:b])
+    assert np.array_equal(got[others], xy0[others])
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_shuffled_one_iteration_parity(name):
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=1)
+    got, tr, done = gpu_layout(g, xy0, **p)
+    ref, E, _ = _oracle(g, xy0, p)
+    assert done == 1
+    assert_positions_close(got, ref, POS_TOL, what=f"{name} shuffled one iteration")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p),
+                        what=f"{name} shuffled one iteration")
+
+
+def test_shuffled_iterations_use_fresh_permutations():
+    """Iteration 1 walks pi_1, not pi_0: shadowed second iteration (from the
+    GPU's state after one iteration, the oracle's second iteration with the
+    cooled step) -- via max_batches inside iteration 1."""
+    g, xy0, cfg = build_config("C3b256")
+    nb = -(-g.n // cfg.batch)
+    s1, _, _ = gpu_layout(g, xy0, **_params(cfg, iters=2, max_batches=nb))
+    s2, _, _ = gpu_layout(g, xy0, **_params(cfg, iters=2, max_batches=nb + 1))
+    members = oracle.permutation(g.n, SEED, 1)[:cfg.batch]
+    f = oracle.forces(g.n, g.rowptr, g.colidx, s1, 0, g.n)[members]
+    ref = s1.astype(np.float64).copy()
+    ref[members] += cfg.cooling * f / np.hypot(f[:, 0], f[:, 1])[:, None]
+    assert_positions_close(s2, ref, POS_TOL_BATCH, what="iteration 1, first batch (pi_1)")
+    others = np.setdiff1d(np.arange(g.n), members)
+    assert np.array_equal(s2[others], s1[others])
+
+
+def test_seed_zero_is_the_sequential_path_bitwise():
+    g, xy0, cfg = build_config("C2")
+    a, ea, _ = gpu_layout(g, xy0, iters=2, batch=cfg.batch)
+    b, eb, _ = gpu_layout(g, xy0, iters=2, batch=cfg.batch, shuffle_seed=0)
+    assert np.array_equal(a, b) and np.array_equal(ea, eb)
+
+
+def test_shuffled_b_equals_n_matches_sequential_positions_bitwise():
+    """b = n: every force sees the frozen state and each target's sums run in
+    the same order whatever its batch position, so the randomised run moves
+    every vertex to the same bytes (the energy sum order differs)."""
+    g = grid_graph(30, 37)
+    xy0 = uniform_coords(g.n, 19)
+    a, ea, _ = gpu_layout(g, xy0, iters=3, batch=g.n)
+    b, eb, _ = gpu_layout(g, xy0, iters=3, batch=g.n, shuffle_seed=SEED)
+    assert np.array_equal(a, b)
+    np.testing.assert_allclose(ea, eb, rtol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_shuffled_determinism_bitwise(name):
+    g, xy0, cfg = build_config(name)
+    p = _params(cfg, iters=3)
+    a, ea, _ = gpu_layout(g, xy0, **p)
+    b, eb, _ = gpu_layout(g, xy0, **p)
+    assert np.array_equal(a, b) and np.array_equal(ea, eb)
+
+
+def test_shuffled_driver_and_rejections():
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0, cfg = build_config("C5")
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=1, batch=1024, max_batches=2, shuffle_seed=SEED)
+        torch.cuda.synchronize()
+        assert bl.bl_driver_name(lay.h) == "two-barrier"
+        assert bl.bl_last_launch_count(lay.h) == 1
+        for bad in (dict(batch=4096, shuffle_seed=1), dict(algo=bl.BL_ALGO_BH, shuffle_seed=1)):
+            with pytest.raises(bl.BLError) as ei:
+                lay.layout_device(d, iters=1, **bad)
+            assert ei.value.status == bl.BL_EINVAL
