@@ -81,16 +81,17 @@ def test_seed_zero_is_the_sequential_path_bitwise():
     assert np.array_equal(a, b) and np.array_equal(ea, eb)
 
 
-def test_shuffled_b_equals_n_matches_sequential_positions_bitwise():
-    """b = n: every force sees the frozen state and each target's sums run in
-    the same order whatever its batch position, so the randomised run moves
-    every vertex to the same bytes (the energy sum order differs)."""
+def test_shuffled_b_equals_n_matches_sequential():
+    """b = n: every force sees the frozen state, so the visiting order
+    changes only rounding (a target's batch position decides which of the
+    kernel's reciprocal forms -- paired or single, DESIGN.md §4 -- its pairs
+    use) and the order of the energy sum."""
     g = grid_graph(30, 37)
     xy0 = uniform_coords(g.n, 19)
     a, ea, _ = gpu_layout(g, xy0, iters=3, batch=g.n)
     b, eb, _ = gpu_layout(g, xy0, iters=3, batch=g.n, shuffle_seed=SEED)
-    assert np.array_equal(a, b)
-    np.testing.assert_allclose(ea, eb, rtol=1e-6)
+    assert_positions_close(b, a, POS_TOL, what="b = n shuffled vs sequential")
+    assert_energy_close(eb[:1], ea[:1], tol=2e-6, what="b = n shuffled vs sequential")
 
 
 @pytest.mark.parametrize("name", ["C1", "C4"])
