@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--members", type=int, default=12)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--iters", type=int, default=0, help="0: the config's")
+    ap.add_argument("--out", default="", help="output directory (default tests/golden)")
     args = ap.parse_args()
     g, xy0, cfg = build_config(args.config)
     iters = args.iters or cfg.iters
@@ -73,7 +74,8 @@ def main():
         "oracle_f64": E.tolist(), "ensemble_f64": ens, "oracle_f32": E32.tolist(),
         "seconds": time.time() - t0, "threads": oracle.max_threads() if not args.threads else args.threads,
     }
-    path = os.path.join(ROOT, "tests", "golden", f"energy_{args.config}.json")
+    path = os.path.join(args.out or os.path.join(ROOT, "tests", "golden"),
+                        f"energy_{args.config}.json")
     with open(path, "w") as fh:
         json.dump(out, fh)
     print("wrote", path, flush=True)
