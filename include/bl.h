@@ -227,6 +227,17 @@ bl_status bl_microbench(double rates[4]);
  * Copies up to len values; returns how many (0 if profiling is off). */
 int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t len);
 
+/* Debug aid for the CHECKED build of the library (libbl_checked.so, built
+ * with -DBL_CHECKED): every cross-CTA value of the exact
+ * whole-GPU kernel carries the batch it comes from, and readers check it
+ * (Alg. 2's frozen-batch semantics), plus bounds and protocol
+ * invariants; BL_JITTER=<seed> adds seeded random sleeps at task boundaries.
+ * Copies the violation record of the last launch on h into out[8]: out[0] =
+ * violations, out[1] = first code, out[2..4] = its details.  Synchronises h's
+ * last stream.  Returns 1 (checked build), 0 (production build: nothing is
+ * recorded, out zeroed) or -1 (NULL argument / CUDA error). */
+int32_t bl_debug_check(bl_ctx *h, uint32_t *out);
+
 void bl_destroy(bl_ctx *h);
 const char *bl_status_string(bl_status s);
 const char *bl_last_error(const bl_ctx *h);

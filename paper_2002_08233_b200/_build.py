@@ -80,5 +80,20 @@ def build(force: bool = False, verbose: bool = False, so: str = SO, extra_flags=
     return so
 
 
+CHECKED_SO = os.path.join(HERE, "libbl_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The checked build (-DBL_CHECKED): phase stamps on every
+    cross-CTA value, invariant checks, seeded schedule jitter.  Test
+    infrastructure for the memory-ordering evidence; same sources."""
+    if not force and os.path.exists(CHECKED_SO) and os.path.getmtime(CHECKED_SO) >= max(
+            os.path.getmtime(f) for f in _inputs()):
+        return CHECKED_SO
+    return build(force=True, so=CHECKED_SO, extra_flags=["-DBL_CHECKED"])
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    if "--checked" in sys.argv:
+        build_checked(force=True)

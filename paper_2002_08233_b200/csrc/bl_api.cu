@@ -90,6 +90,25 @@ extern "C" int32_t bl_last_launch_count(const bl_ctx *h) { return h ? h->launche
 
 extern "C" const char *bl_driver_name(const bl_ctx *h) { return h ? h->driver_last : ""; }
 
+// Checked builds (libbl_checked.so, -DBL_CHECKED): copy the
+// violation record of the last exact whole-GPU launch (out[0] = violations,
+// out[1] = first code, out[2..4] = its details).  Returns 1 in a checked
+// build, 0 in the production library (nothing recorded), -1 on error.
+extern "C" int32_t bl_debug_check(bl_ctx *h, uint32_t *out) {
+  if (!h || !out) return -1;
+#ifdef BL_CHECKED
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  if (!h->d_chk) return 1;
+  if (cudaStreamSynchronize(h->last_stream) != cudaSuccess) return -1;
+  if (cudaMemcpy(out, h->d_chk, sizeof(unsigned) * 5, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return 1;
+#else
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  return 0;
+#endif
+}
+
 extern "C" const char *bl_kernel_name(const bl_ctx *h) {
   return h ? (h->kname_last[0] ? h->kname_last : h->kname) : "";
 }
@@ -314,6 +333,10 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_cellf);
   cudaFree(h->d_nleaf);
   cudaFree(h->d_leafv);
+  cudaFree(h->d_chk);
+  cudaFree(h->d_part_st);
+  cudaFree(h->d_pend_st);
+  cudaFree(h->d_xy_st);
   delete h;
 }
 
@@ -435,6 +458,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
 
   k.red_cap = red_cap_for(k.chunk4);
   k.guided = env_int("BL_GUIDED", 2);
+  k.min_unit4 = std::max(1, env_int("BL_MIN_UNIT4", BL_MIN_UNIT4));
   model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
   // very large batches (b n >= 5e8 pairs, e.g. 2^20 vertices x 1024) amortise
   // the fewer, wider warps of <256,16,6> best; below, <512,8,2> (measured)
@@ -452,6 +476,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   const int async_env = env_int("BL_ASYNC", -1);
   const bool async_auto = (long long)b * n >= (1LL << 22);
   if (k.pipelined && (async_env == 1 || (async_env < 0 && async_auto)) &&
+      (b + 32 * vt->T - 1) / (32 * vt->T) <= BL_NTT_MAX &&
       k.red_cap / 2 / (((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T) >= 2) {
     k.pipelined = 2;
     k.part_nbuf = 3;
@@ -468,6 +493,26 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     const int tile_slots = ((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T;
     k.red_cap = std::min(k.red_cap, 2 * k.nsub_max * tile_slots);
   }
+#ifdef BL_CHECKED
+  // checked build: zeroed violation record and stamps for this launch
+  if (!h->d_chk) {
+    if (cudaMalloc((void **)&h->d_chk, sizeof(unsigned) * 8) != cudaSuccess ||
+        cudaMalloc((void **)&h->d_xy_st, sizeof(unsigned) * (size_t)n) != cudaSuccess)
+      return bl_fail(h, BL_ENOMEM, "checked-build buffers");
+  }
+  if ((s = grow(h, h->d_part_st, h->part_st_cap, (size_t)3 * b * G)) != BL_OK) return s;
+  if ((s = grow(h, h->d_pend_st, h->pend_st_cap, (size_t)2 * b)) != BL_OK) return s;
+  BL_CUDA(h, cudaMemsetAsync(h->d_chk, 0, sizeof(unsigned) * 8, st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_xy_st, 0, sizeof(unsigned) * (size_t)n, st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_part_st, 0, sizeof(unsigned) * h->part_st_cap, st));
+  BL_CUDA(h, cudaMemsetAsync(h->d_pend_st, 0, sizeof(unsigned) * h->pend_st_cap, st));
+  k.chk = h->d_chk;
+  k.part_st = h->d_part_st;
+  k.pend_st = h->d_pend_st;
+  k.xy_st = h->d_xy_st;
+  k.jitter = (unsigned)env_int("BL_JITTER", 0);
+  k.chk_break = env_int("BL_CHK_BREAK", 0);
+#endif
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   h->driver_last = forces_mode ? "two-barrier"

@@ -63,6 +63,9 @@ struct bl_ctx {
   unsigned *d_aflag = nullptr;
   float2 *d_cellf = nullptr;  // BH per-iteration precomputation
   int *d_nleaf = nullptr, *d_leafv = nullptr;
+  // checked builds (-DBL_CHECKED): violation record and phase stamps
+  unsigned *d_chk = nullptr, *d_part_st = nullptr, *d_pend_st = nullptr, *d_xy_st = nullptr;
+  size_t part_st_cap = 0, pend_st_cap = 0;
   // quality-metric scratch (allocated per call)
 };
 

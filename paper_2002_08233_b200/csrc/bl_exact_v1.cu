@@ -7,5 +7,8 @@ extern const BLVariant bl_exact_v1[] = {
     {512, 8, 3, (void *)bl_layout_kernel<512, 8, 3>},
     {512, 8, 4, (void *)bl_layout_kernel<512, 8, 4>},
     {512, 4, 2, (void *)bl_layout_kernel<512, 4, 2>},
+    {512, 4, 1, (void *)bl_layout_kernel<512, 4, 1>},
+    {512, 2, 1, (void *)bl_layout_kernel<512, 2, 1>},
+    {512, 1, 1, (void *)bl_layout_kernel<512, 1, 1>},
 };
-extern const int bl_exact_v1_count = 3;
+extern const int bl_exact_v1_count = 6;

@@ -62,12 +62,13 @@ struct BLUnits {
 // Precondition with a dirty range: red_cap holds >= 2 sub-ranges of every
 // tile (the host's driver eligibility checks; tests/cpp/test_units.cu).
 __host__ __device__ inline BLUnits bl_units(int bt, int T, int clean4, bool dirty, int red_cap,
-                                            int nsub_max = BL_NSUB_MAX) {
+                                            int nsub_max = BL_NSUB_MAX,
+                                            int min_unit4 = BL_MIN_UNIT4) {
   BLUnits u;
   u.ntt = (bt + 32 * T - 1) / (32 * T);
   int cap = red_cap / (u.ntt * 32 * T);
   if (cap > nsub_max) cap = nsub_max;
-  int nc = clean4 / BL_MIN_UNIT4;
+  int nc = clean4 / (min_unit4 > 0 ? min_unit4 : 1);
   if (nc > cap - (dirty ? 1 : 0)) nc = cap - (dirty ? 1 : 0);
   u.nc = nc < 1 ? 1 : nc;
   u.nsub = u.nc + (dirty ? 1 : 0);
@@ -107,6 +108,7 @@ struct BLKParams {
   int red_cap;           // float2 slots of the shared partial buffer
   int guided;            // sub-range size profile (bl_guided_start)
   int nsub_max;          // async driver: sub-ranges per target tile (incl. the dirty one)
+  int min_unit4;         // pipelined / async: minimum float4 slots per clean sub-range
   unsigned spin_max;     // async driver: longest back-off sleep of a waiting warp (ns)
   // (a, r)-energy model (reading C15): attraction d^a/K, repulsion C K^2 d^r;
   // amode 0..3: a = 2, 1, 0, 3 (no pow), 4: general; rmode 0: r = -1, 1: general
@@ -133,6 +135,14 @@ struct BLKParams {
   int *iters_done;
   unsigned *bar;
   float2 *f_out;
+  // checked builds (-DBL_CHECKED, libbl_checked.so): violation
+  // record chk[0] = count, chk[1] = first code, chk[2..4] = its details;
+  // phase stamps of every cross-CTA value (part, pend, committed xy);
+  // jitter != 0 inserts seeded random sleeps at task boundaries
+  unsigned *chk, *part_st, *pend_st, *xy_st;
+  unsigned jitter;
+  int chk_break;         // checked builds: 1 = skip the barrier wait of the control
+                         // task (fault injection proving the checks are live)
   // optional phase profile (nullptr = off): [0..7] CTA-0 phase cycle sums,
   // [8 + c] CTA c's cycles from phase-R start to barrier-1 arrival
   unsigned long long *prof;
@@ -160,6 +170,53 @@ __device__ __forceinline__ float bl_rsqrt(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// ---- checked builds: invariant and phase-stamp checks (compiled out otherwise)
+#ifdef BL_CHECKED
+static __device__ __noinline__ void bl_chk_fail(const BLKParams &p, unsigned code, unsigned a, unsigned b) {
+  atomicAdd(p.chk, 1u);
+  if (atomicCAS(p.chk + 1, 0u, code) == 0u) {
+    p.chk[2] = a;
+    p.chk[3] = b;
+    p.chk[4] = blockIdx.x;
+  }
+}
+#define BL_CHK(cond, code, a, b)                                 \
+  do {                                                           \
+    if (!(cond)) bl_chk_fail(p, (code), (unsigned)(a), (unsigned)(b)); \
+  } while (0)
+#define BL_CHK_ON 1
+// seeded random sleep (0..2 us, probability 1/4) at a task boundary: shakes
+// the interleaving of warps and CTAs; results must stay bitwise identical
+__device__ __forceinline__ void bl_jitter(const BLKParams &p, unsigned salt) {
+  if (!p.jitter) return;
+  unsigned long long t = clock64();
+  unsigned long long z = ((unsigned long long)p.jitter << 32) ^ (t * 0x9E3779B97F4A7C15ull) ^
+                         ((unsigned long long)blockIdx.x << 20) ^ (threadIdx.x >> 5) ^ salt;
+  z ^= z >> 29;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 32;
+  if ((z & 3ull) == 0ull) __nanosleep((unsigned)((z >> 8) & 2047ull));
+}
+#else
+#define BL_CHK(cond, code, a, b) \
+  do {                           \
+  } while (0)
+#define BL_CHK_ON 0
+__device__ __forceinline__ void bl_jitter(const BLKParams &, unsigned) {}
+#endif
+// violation codes
+enum {
+  BLC_PART_STAMP = 1,   // an update read a partial not from its batch
+  BLC_PEND_STAMP = 2,   // a neighbour coordinate from pend not from batch q-1
+  BLC_XY_STAMP = 3,     // a neighbour coordinate from xy not the last committed one
+  BLC_TGT_STAMP = 4,    // a staged target not the last committed coordinate
+  BLC_DIRTY_EARLY = 5,  // a dirty unit started before this CTA's updates
+  BLC_TOKENS = 6,       // more completion tokens than the phase needs
+  BLC_BOUNDS = 7,       // index out of range (part / pend / red / src)
+  BLC_PHASEU_STAMP = 8, // two-barrier phase U read a partial not from its batch
+  BLC_SLOT_GEN = 9      // async: a phase entered a slot not released for it
+};
+
 // ---- batch randomisation (§4.3.3; readings R1-R2 of DESIGN.md §3):
 // pi_it is a 4-round Feistel bijection of [0, 2^(2h)) keyed from splitmix64,
 // restricted to [0, n) by cycle walking -- integer arithmetic only, so any
@@ -418,10 +475,11 @@ __host__ __device__ inline BLGeom bl_geom(int c, int G, int n, int k_lo, int own
 template <int T, int TP>
 __device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, const float4 *src4,
                                            const float2 *tgt, float2 *red, float2 *part, int g,
-                                           const BLUnits &U, const BLGeom &geo) {
+                                           const BLUnits &U, const BLGeom &geo, int tag = 0) {
   const int G = gridDim.x, c = blockIdx.x;
   const int lane = threadIdx.x & 31;
   const int tile = g % U.ntt, sub = g / U.ntt;
+  BL_CHK(geo.last4 <= p.chunk4, BLC_BOUNDS, 10, geo.last4);
   float tx[T], ty[T];
   bl_f2 AX[T], AY[T];
 #pragma unroll
@@ -453,10 +511,17 @@ __device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, c
     f2unpack(AY[k], ay0, ay1);
     const float2 r = make_float2(ax0 + ax1, ay0 + ay1);
     if (idx < bt) {
-      if (U.nsub == 1)
+      if (U.nsub == 1) {
         part[(size_t)idx * G + c] = r;
-      else
+        if (BL_CHK_ON) {
+          const size_t o = (size_t)(part - p.part) + (size_t)idx * G + c;
+          BL_CHK(o < (size_t)p.part_nbuf * p.b * G, BLC_BOUNDS, 1, o);
+          p.part_st[o] = (unsigned)tag + 1u;
+        }
+      } else {
+        BL_CHK(sub * (U.ntt * 32 * T) + idx < p.red_cap, BLC_BOUNDS, 2, sub);
         red[sub * (U.ntt * 32 * T) + idx] = r;
+      }
     }
   }
 }
@@ -465,7 +530,7 @@ __device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, c
 // CTA barrier).
 template <int T>
 __device__ __forceinline__ void bl_combine(const BLKParams &p, int bt, const float2 *red,
-                                           float2 *part, const BLUnits &U) {
+                                           float2 *part, const BLUnits &U, int tag = 0) {
   if (U.nsub <= 1) return;
   const int G = gridDim.x, c = blockIdx.x;
   for (int idx = threadIdx.x; idx < bt; idx += BL_NT) {
@@ -476,6 +541,7 @@ __device__ __forceinline__ void bl_combine(const BLKParams &p, int bt, const flo
       acc.y += v.y;
     }
     part[(size_t)idx * G + c] = acc;
+    if (BL_CHK_ON) p.part_st[(size_t)(part - p.part) + (size_t)idx * G + c] = (unsigned)tag + 1u;
   }
 }
 
@@ -486,7 +552,8 @@ __device__ __forceinline__ void bl_combine(const BLKParams &p, int bt, const flo
 template <int T, int TP>
 __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int bt,
                                                const float4 *src4, const float2 *tgt, float2 *red,
-                                               int *unit_ctr, float2 *part, BLProf &pf) {
+                                               int *unit_ctr, float2 *part, BLProf &pf,
+                                               int tag = 0) {
   const int G = gridDim.x, c = blockIdx.x;
   const int lane = threadIdx.x & 31;
   const BLGeom geo = bl_geom(c, G, p.n, 0, 0);
@@ -497,14 +564,21 @@ __device__ __forceinline__ void bl_sweep_units(const BLKParams &p, int lo, int b
     if (lane == 0) g = atomicAdd(unit_ctr, 1);
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g >= nunits) break;
-    bl_do_unit<T, TP>(p, lo, bt, src4, tgt, red, part, g, U, geo);
+    bl_do_unit<T, TP>(p, lo, bt, src4, tgt, red, part, g, U, geo, tag);
   }
   pf.mark(1);
   __syncthreads();
-  bl_combine<T>(p, bt, red, part, U);
+  bl_combine<T>(p, bt, red, part, U, tag);
 }
 
 // ---------------------------------------------------------------- phase R
+__device__ __forceinline__ unsigned bl_exp_stamp(const BLKParams &p, int j, int qmax) {
+  // stamp of the latest batch index L <= qmax containing j (sequential
+  // batches: batch of j = j / b), + 1; 0 if none
+  const int tj = j / p.b;
+  const int L = qmax - (((qmax - tj) % p.nb) + p.nb) % p.nb;
+  return L >= 0 ? (unsigned)L + 1u : 0u;
+}
 // Attraction items of a RANDOMISED batch (readings R1-R2): batch position k
 // holds vertex pi(lo + k), whose items are item_ptr[v] .. item_ptr[v+1]; the
 // batch's items are numbered through ioff[k] = sum_{k' < k} items(pi(lo+k'))
@@ -547,14 +621,19 @@ __device__ __forceinline__ void bl_batch_item_offsets(const BLKParams &p, const 
 template <int T, int TP>
 __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, const float4 *src4,
                                            float2 *tgt, float2 *red, int *unit_ctr, BLProf &pf,
-                                           const BLPerm &P, int *ioff) {
+                                           const BLPerm &P, int *ioff, int tag = 0) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool tgt_smem = bt <= BL_TGT_CAP;
 
   // (0) stage the batch's targets (frozen coordinates)
   if (tgt_smem && !p.attr_only)
-    for (int i = threadIdx.x; i < bt; i += BL_NT) tgt[i] = __ldcg(p.xy + bl_perm(P, lo + i));
+    for (int i = threadIdx.x; i < bt; i += BL_NT) {
+      tgt[i] = __ldcg(p.xy + bl_perm(P, lo + i));
+      if (BL_CHK_ON && !P.on && !p.forces_mode)
+        BL_CHK(__ldcg(p.xy_st + lo + i) == bl_exp_stamp(p, lo + i, tag - 1), BLC_TGT_STAMP, tag,
+               lo + i);
+    }
 
   // (1r) randomised batch: items through pi and the batch item offsets
   if (P.on) {
@@ -635,7 +714,12 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
       }
       float2 cj[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) cj[u] = jj[u] >= 0 ? __ldcg(p.xy + jj[u]) : ci;
+      for (int u = 0; u < 4; ++u) {
+        cj[u] = jj[u] >= 0 ? __ldcg(p.xy + jj[u]) : ci;
+        if (BL_CHK_ON && jj[u] >= 0 && !p.forces_mode)
+          BL_CHK(__ldcg(p.xy_st + jj[u]) == bl_exp_stamp(p, jj[u], tag - 1), BLC_XY_STAMP, tag,
+                 jj[u]);
+      }
       auto scan_row = [&](auto fast) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -660,7 +744,8 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
 
   // (2) repulsion sweep over the CTA's resident sources
   if (!p.attr_only)
-    bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, pf);
+    bl_sweep_units<T, TP>(p, lo, bt, src4, tgt_smem ? tgt : nullptr, red, unit_ctr, p.part, pf,
+                          tag);
   pf.mark(2);
 }
 
@@ -676,7 +761,7 @@ __device__ __forceinline__ void bl_phase_R(const BLKParams &p, int lo, int bt, c
 // barrier (bl_refresh_resident).
 __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, double stepd,
                                            float4 *src4, double &e_acc, const BLPerm &P,
-                                           const int *ioff) {
+                                           const int *ioff, int tag = 0) {
   const int G = gridDim.x, c = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v0 = P.on ? c : lo + ((c - lo % G) + G) % G;
@@ -696,6 +781,10 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
         rx += q.x;
         ry += q.y;
       }
+      if (BL_CHK_ON)
+        for (int cc = lane; cc < G; cc += 32)
+          BL_CHK(__ldcg(p.part_st + (size_t)local * G + cc) == (unsigned)tag + 1u,
+                 BLC_PHASEU_STAMP, tag, cc);
     }
     float sx = 0.f, sy = 0.f;
     for (int a = a0 + lane; a < a1; a += 32) {
@@ -724,6 +813,7 @@ __device__ __forceinline__ void bl_phase_U(const BLKParams &p, int lo, int bt, d
           p.xy[v] = cv;
           if (!P.on) bl_src_set(src4, (v - c) / G, cv);
         }
+        if (BL_CHK_ON) p.xy_st[v] = (unsigned)tag + 1u;
         e_acc += q;
       }
     }
@@ -788,6 +878,9 @@ struct BLShared {
   double e_task[BL_ETASK_MAX];
   double e_warp[BL_NW_MAX];
   int ioff[BL_TGT_CAP + 1];  // randomised batches: item offsets per position
+#ifdef BL_CHECKED
+  int chk_upd[BL_ETASK_MAX];   // batch (+1) whose update task t last finished
+#endif
   unsigned long long pkey[4];  // randomised batches: round keys of pi_it
   // CSR rows (<= 32 entries) of this CTA's owned vertices of a batch, staged
   // by the control task of the phase that sweeps the batch, used by the
@@ -848,7 +941,10 @@ __device__ __forceinline__ void bl_commit_warp(const BLKParams &p, int q, const 
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b, hi = min(lo + p.b, p.n);
   const int v0 = lo + ((c - lo % G) + G) % G;
-  for (int v = v0 + lane * G; v < hi; v += 32 * G) p.xy[v] = bl_src_get(src4, (v - c) / G);
+  for (int v = v0 + lane * G; v < hi; v += 32 * G) {
+    p.xy[v] = bl_src_get(src4, (v - c) / G);
+    if (BL_CHK_ON) p.xy_st[v] = (unsigned)q + 1u;
+  }
 }
 
 // Energy of iteration `it` from the per-CTA sums, warp-cooperative, in a
@@ -860,6 +956,22 @@ __device__ __forceinline__ double bl_energy_sum_warp(const BLKParams &p, int it)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
   return __shfl_sync(0xffffffffu, e, 0);
+}
+
+// Checked builds: the coordinate of neighbour j read by the update of batch q
+// must be exactly the one Alg. 2 prescribes (frozen batches):
+// batch q-1's new value from pend, else the last COMMITTED update of j --
+// batch L = the latest index <= q-2 of j's batch (sequential batches) -- or
+// none (stamp 0).  Not older (a lost commit) and not newer.
+__device__ __forceinline__ void bl_chk_nb(const BLKParams &p, int q, int j, int plo, int phi) {
+#ifdef BL_CHECKED
+  if (j >= plo && j < phi) {
+    BL_CHK(__ldcg(p.pend_st + (size_t)((q - 1) & 1) * p.b + (j - plo)) == (unsigned)q,
+           BLC_PEND_STAMP, q, j);
+  } else {
+    BL_CHK(__ldcg(p.xy_st + j) == bl_exp_stamp(p, j, q - 2), BLC_XY_STAMP, q, j);
+  }
+#endif
 }
 
 // Update of one owned vertex v of batch q (warp-cooperative); ||f||^2 -> *eq.
@@ -885,6 +997,10 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     rx += t.x;
     ry += t.y;
   }
+  if (BL_CHK_ON)
+    for (int cc = lane; cc < G; cc += 32)
+      BL_CHK(__ldcg(p.part_st + (size_t)(row - p.part) + cc) == (unsigned)q + 1u, BLC_PART_STAMP,
+             q, cc);
   int k0 = 0, k1 = 0;
   if (!srow) {
     k0 = __ldg(p.rowptr + v);
@@ -897,6 +1013,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       if (lane < sdeg) {
         const int j = srow[lane];
         const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        if (BL_CHK_ON) bl_chk_nb(p, q, j, plo, phi);
         const float dx = cj.x - ci.x, dy = cj.y - ci.y;
         const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
         const float rs = bl_rsqrt(d2);
@@ -916,6 +1033,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       for (int k = k0 + lane; k < k1; k += 32) {
         const int j = __ldg(p.colidx + k);
         const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        if (BL_CHK_ON) bl_chk_nb(p, q, j, plo, phi);
         const float dx = cj.x - ci.x, dy = cj.y - ci.y;
         const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
         const float rs = bl_rsqrt(d2);
@@ -937,6 +1055,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       for (int u = 0; u < 8; ++u) {
         const int j = jj[u];
         cj[u] = j < 0 ? ci : (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        if (BL_CHK_ON && j >= 0) bl_chk_nb(p, q, j, plo, phi);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -968,6 +1087,10 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       bl_src_set(src4, (v - c) / G, cv);
     }
     p.pend[(size_t)(q & 1) * p.b + local] = cv;
+    if (BL_CHK_ON) {
+      BL_CHK(local >= 0 && local < p.b, BLC_BOUNDS, 3, local);
+      p.pend_st[(size_t)(q & 1) * p.b + local] = (unsigned)q + 1u;
+    }
     *eq = qq;
   }
 }
@@ -993,11 +1116,35 @@ __device__ __forceinline__ void bl_stage_rows_warp(const BLKParams &p, int q, BL
   const int v0 = lo + ((c - lo % G) + G) % G;
   const int owned = v0 < hi ? (hi - 1 - v0) / G + 1 : 0;
   const int buf = q & 1;
-  for (int t = 0; t < owned; ++t) {
-    const int v = v0 + t * G;
-    const int k0 = __ldg(p.rowptr + v), deg = __ldg(p.rowptr + v + 1) - k0;
-    if (deg <= 32 && lane < deg) sh.rows[buf][t][lane] = __ldg(p.colidx + k0 + lane);
-    if (lane == 0) sh.rdeg[buf][t] = deg <= 32 ? deg : -1;
+  // two L2 round trips in all (latency is the cost here: this runs on the
+  // per-batch critical path): the row bounds of up to 32 owned vertices in
+  // one load per lane, then the rows of 8 vertices at a time, every load
+  // issued before the first store
+  for (int t0 = 0; t0 < owned; t0 += 32) {
+    int k0 = 0, deg = 0;
+    if (t0 + lane < owned) {
+      const int v = v0 + (t0 + lane) * G;
+      k0 = __ldg(p.rowptr + v);
+      deg = __ldg(p.rowptr + v + 1) - k0;
+    }
+    const int m = min(32, owned - t0);
+    for (int t1 = 0; t1 < m; t1 += 8) {
+      int col[8], dg[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int kk = __shfl_sync(0xffffffffu, k0, (t1 + u) & 31);
+        dg[u] = __shfl_sync(0xffffffffu, deg, (t1 + u) & 31);
+        col[u] = (t1 + u < m && dg[u] <= 32 && lane < dg[u]) ? __ldg(p.colidx + kk + lane) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (t1 + u < m) {
+          const int t = t0 + t1 + u;
+          if (dg[u] <= 32 && lane < dg[u]) sh.rows[buf][t][lane] = col[u];
+          if (lane == 0) sh.rdeg[buf][t] = dg[u] <= 32 ? dg[u] : -1;
+        }
+      }
+    }
   }
   __syncwarp();
   if (lane == 0) sh.rowq[buf] = q;
@@ -1016,7 +1163,10 @@ __device__ __forceinline__ void bl_fence_to_completer(const BLKParams &p) {
 __device__ __forceinline__ void bl_token(const BLKParams &p, BLShared &sh, const BLPhase &f,
                                          int need) {
   // lane 0 of the caller, after its writes were fenced
-  if (atomicAdd(&sh.a_tok[f.ph & 1], 1) != need - 1) return;
+  bl_jitter(p, 11);
+  const int tok = atomicAdd(&sh.a_tok[f.ph & 1], 1);
+  BL_CHK(tok < need, BLC_TOKENS, f.ph, tok);
+  if (tok != need - 1) return;
   __threadfence_block();
   const int G = gridDim.x, c = blockIdx.x;
   if (f.owned > 0) {
@@ -1040,7 +1190,7 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
                                                unsigned bar_target, int need = -1) {
   const int lane = threadIdx.x & 31;
   int go = 0;
-  if (lane == 0 && (int)(bl_ld_acquire(p.bar) - bar_target) >= 0)
+  if (lane == 0 && ((int)(bl_ld_acquire(p.bar) - bar_target) >= 0 || (BL_CHK_ON && p.chk_break)))
     go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
 #ifdef BL_PHASE_TS
   if (go && p.prof) sh.ts_claim = clock64();
@@ -1083,6 +1233,20 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
   // async driver: the targets must have landed before `ready` lets warps
   // into phase ph+1 (the pipelined driver waits at its phase-end barrier)
   if (need >= 0) asm volatile("cp.async.wait_all;" ::: "memory");
+  if (BL_CHK_ON && !stop && f.ph + 1 < f.P) {
+    // the staged targets of batch ph+1 are its last committed coordinates
+    // (from the previous iteration; batch ph+1-nb <= ph-2 was committed by
+    // an earlier control task) -- checked on the bytes that landed
+    const int lo_n = ((f.ph + 1) % nb) * p.b, bt_n = min(p.b, p.n - lo_n);
+    for (int i = lane; i < bt_n; i += 32) {
+      if (need >= 0) {
+        const float2 a = f.tgt_next[i], b = __ldcg(p.xy + lo_n + i);
+        BL_CHK(a.x == b.x && a.y == b.y, BLC_TGT_STAMP, f.ph, lo_n + i);
+      }
+      BL_CHK(__ldcg(p.xy_st + lo_n + i) == bl_exp_stamp(p, lo_n + i, f.ph - 2), BLC_TGT_STAMP,
+             f.ph, lo_n + i);
+    }
+  }
   __syncwarp();
   if (lane == 0) {
     if (stop) *(volatile int *)&sh.stop_flag = 1;
@@ -1110,10 +1274,14 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
   const int buf = f.q1 & 1;
   const volatile BLShared &vsh = sh;
   const bool staged = vsh.rowq[buf] == f.q1 && vsh.rdeg[buf][t] >= 0;
+  bl_jitter(p, 21);
   bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t],
                 staged ? sh.rows[buf][t] : nullptr, staged ? vsh.rdeg[buf][t] : 0);
   __syncwarp();
   if (lane == 0) {
+#ifdef BL_CHECKED
+    sh.chk_upd[t] = f.q1 + 1;
+#endif
     __threadfence_block();
 #ifdef BL_PHASE_TS
     if (atomicAdd(&sh.u_done, 1) == f.owned - 1 && p.prof) sh.ts_upd = clock64();
@@ -1136,11 +1304,12 @@ __device__ __forceinline__ void bl_phase_tasks(const BLKParams &p, const BLPhase
   const int bt = has_R ? min(p.b, p.n - lo) : 0;
   const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
   BLUnits U = {1, 0, 0};
-  if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, p.red_cap);
+  if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, p.red_cap, BL_NSUB_MAX, p.min_unit4);
   const int n_all = has_R ? U.ntt * U.nsub : 0;
   const int n_clean = has_R ? U.ntt * U.nc : 0;
   float2 *part = p.part + (size_t)(f.ph & 1) * p.b * G;
   for (;;) {
+    bl_jitter(p, 27);
     if (f.ph > 0 && vs.ready != f.ph) bl_try_control(p, f, src4, sh, bar_target);
     if (bl_try_update(p, f, src4, sh)) continue;
     int g = n_all;
@@ -1158,8 +1327,14 @@ __device__ __forceinline__ void bl_phase_tasks(const BLKParams &p, const BLPhase
           __nanosleep(64);
         }
         __threadfence_block();
+#ifdef BL_CHECKED
+        if (!vs.stop_flag)
+          for (int t = 0; t < f.owned; ++t)
+            BL_CHK(((volatile int *)sh.chk_upd)[t] == f.q1 + 1, BLC_DIRTY_EARLY, f.ph, t);
+#endif
       }
-      bl_do_unit<T, TP>(p, lo, bt, src4, tgt, red, part, g, U, geo);
+      bl_jitter(p, 24);
+      bl_do_unit<T, TP>(p, lo, bt, src4, tgt, red, part, g, U, geo, f.ph);
       continue;
     }
     // nothing left to grab: done once control ran and every update is taken
@@ -1232,8 +1407,9 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
     if (ph < P) {
       const int lo = (ph % nb) * p.b, bt = min(p.b, p.n - lo);
       const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
-      const BLUnits U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, p.red_cap);
-      bl_combine<T>(p, bt, red, p.part + (size_t)(ph & 1) * p.b * G, U);
+      const BLUnits U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, p.red_cap, BL_NSUB_MAX,
+                                 p.min_unit4);
+      bl_combine<T>(p, bt, red, p.part + (size_t)(ph & 1) * p.b * G, U, ph);
     }
     if (threadIdx.x == 0 && f.owned > 0) {
       double e = sh.e_acc;
@@ -1246,6 +1422,7 @@ __device__ __forceinline__ void bl_run_pipelined(const BLKParams &p, float4 *src
     }
     pf.mark(2);
     asm volatile("cp.async.wait_all;" ::: "memory");
+    bl_jitter(p, 28);
     if (ph <= P) bl_grid_arrive(p.bar, bar_target, sh, p.prof != nullptr);
     pf.mark(5);
   }
@@ -1289,10 +1466,15 @@ __device__ __forceinline__ bool bl_try_update_a(const BLKParams &p, const BLPhas
   __threadfence_block();  // acquire the control warp's publication
   const int buf = f.q1 & 1;
   const bool staged = vs.rowq[buf] == f.q1 && vs.rdeg[buf][t] >= 0;
+  bl_jitter(p, 22);
   bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t],
                 staged ? sh.rows[buf][t] : nullptr, staged ? vs.rdeg[buf][t] : 0);
   __syncwarp();
   if (lane == 0) {
+#ifdef BL_CHECKED
+    sh.chk_upd[t] = f.q1 + 1;
+#endif
+    bl_jitter(p, 23);
     bl_fence_to_completer(p);  // pend (read by other CTAs after barrier ph)
     if (atomicAdd(&sh.a_udone[s], 1) == f.owned - 1) {
       __threadfence_block();
@@ -1390,6 +1572,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
       BL_WT(0);
       if (stop) break;
       __threadfence_block();
+      BL_CHK(vs.a_gen[s] == ph, BLC_SLOT_GEN, ph, vs.a_gen[s]);
     }
     prev_owned = f.owned;
 
@@ -1398,7 +1581,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
     const int bt = has_R ? min(p.b, p.n - lo) : 0;
     const BLGeom geo = bl_geom(c, G, p.n, f.owned > 0 ? (f.v0 - c) / G : 0, f.owned);
     BLUnits U = {1, 0, 0};
-    if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, half, p.nsub_max);
+    if (has_R) U = bl_units(bt, T, geo.clean4, geo.d_lo < geo.d_hi, half, p.nsub_max, p.min_unit4);
     const int n_all = has_R ? U.ntt * U.nsub : 0;
     const int n_clean = has_R ? U.ntt * U.nc : 0;
     const int need = (has_R ? U.ntt : 0) + (ph > 0 ? 1 : 0) + f.owned;
@@ -1415,6 +1598,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
         break;
       }
       BL_WT(1);
+      bl_jitter(p, 26);
       if (control()) {
         BL_WT(6);
         idle_ns = 32;
@@ -1454,9 +1638,14 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
           BL_WT(2);
           if (stop) break;
           __threadfence_block();
+#ifdef BL_CHECKED
+          for (int t = 0; t < f.owned; ++t)
+            BL_CHK(((volatile int *)sh.chk_upd)[t] == f.q1 + 1, BLC_DIRTY_EARLY, ph, t);
+#endif
         }
         BL_WT(1);
-        bl_do_unit<T, TP>(p, lo, bt, src4, tgt_s, red_s, part, g, U, geo);
+        bl_jitter(p, 25);
+        bl_do_unit<T, TP>(p, lo, bt, src4, tgt_s, red_s, part, g, U, geo, ph);
         BL_WT(3);
         const int tile = g % U.ntt;
         __syncwarp();
@@ -1481,6 +1670,8 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
                   acc.y += v.y;
                 }
                 part[(size_t)idx * G + c] = acc;
+                if (BL_CHK_ON)
+                  p.part_st[(size_t)(part - p.part) + (size_t)idx * G + c] = (unsigned)ph + 1u;
               }
             }
           }
@@ -1609,10 +1800,10 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b;
       const int bt = min(p.b, p.n - lo);
-      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, unit_ctr, pf, P, sh.ioff);
+      bl_phase_R<T, TP>(p, lo, bt, src4, tgt, red, unit_ctr, pf, P, sh.ioff, batches);
       bl_grid_sync(p.bar, bar_target, unit_ctr);
       pf.mark(3);
-      bl_phase_U(p, lo, bt, step, src4, e_acc, P, sh.ioff);
+      bl_phase_U(p, lo, bt, step, src4, e_acc, P, sh.ioff, batches);
       pf.mark(4);
       ++batches;
       const bool last = (t == p.nb - 1);
