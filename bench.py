@@ -371,6 +371,9 @@ def bench_ours(args, name, g, xy0, cfg, rank, world, local_rank):
     if not args.no_bh:
         line["bh"] = bench_bh(args, lay, d_xy0, params, stream, flush, g, cfg, t_step)
     line["attraction"] = bench_attraction(lay, d_xy0, params, stream, flush, g, peaks)
+    if not args.no_metrics:
+        line["metrics"] = bench_metrics(lay, d_xy, g, peaks, clocks.get("sm_mhz") or sm_max, nsm,
+                                        stream)
     if not args.no_shuffle and cfg.batch <= 2048:
         line["shuffle"] = bench_shuffle(args, lay, d_xy0, params, stream, flush, cfg, t_step)
     if args.latency_configs and args.r == -1.0:
@@ -502,6 +505,58 @@ def bench_shuffle(args, lay, d_xy0, params, stream, flush, cfg, t_default):
             "cost_vs_default": t_shuf / t_default, "cost_of_reshuffle_alone": t_shuf / t_seq2}
 
 
+def bench_metrics(lay, d_xy, g, peaks, sm_mhz, nsm, stream, sources=1024):
+    """Secondary object: the §3.7 quality metrics on the bench's
+    final layout, each with a stated roofline fraction:
+      EU: 2 passes x (4 nnz + 4 (n+1) + 8 n) algorithmic bytes vs HBM;
+      stress: bit-parallel BFS (64 sources per word) -- bytes = 12 B per CSR
+        entry examined + 24 B per vertex per level (visited, next, rowptr) vs
+        HBM, and TEPS (sources x nnz / t, the Graph500 convention);
+      NP: ~5 (n-1) squared-distance evaluations per query (4 radix-select
+        passes + the tie count), 5 FP32 ops each, vs the FP32 lane peak.
+    Timed with CUDA events around the (synchronous) C-ABI calls, after one
+    warm-up call (the scratch is allocated once per context)."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    hbm = float(peaks.get("hbm_gbs", 6540.2)) * 1e9
+    rng = np.random.default_rng(0)
+    src = rng.choice(g.n, min(sources, g.n), replace=False).astype(np.int32)
+
+    def timed(fn, reps):
+        fn()
+        ms = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r = fn()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        return r, float(np.median(ms)) / 1e3
+
+    eu, t_eu = timed(lambda: bl.bl_edge_uniformity(lay.h, d_xy, stream), 5)
+    eu_bytes = 2.0 * (4 * g.nnz + 4 * (g.n + 1) + 8 * g.n)
+    st, t_st = timed(lambda: bl.bl_stress(lay.h, d_xy, src, stream), 2)
+    levels, examined = bl.bl_debug_counters(lay.h)
+    st_bytes = 12.0 * examined + 24.0 * g.n * levels
+    npv, t_np = timed(lambda: bl.bl_neighborhood_preservation(lay.h, d_xy, None, stream), 2)
+    evals = 5.0 * (g.n - 1) * g.n
+    fp32_evals = nsm * 128 * sm_mhz * 1e6 / 5.0
+    return {
+        "layout": "the bench's final layout",
+        "edge_uniformity": {"value": eu, "us": 1e6 * t_eu, "algorithmic_bytes": eu_bytes,
+                            "GB_per_s": eu_bytes / t_eu / 1e9, "frac_of_hbm_peak": eu_bytes / t_eu / hbm},
+        "stress": {"value": st[0], "sources": int(src.size), "ms": 1e3 * t_st,
+                   "pairs": int(st[2]), "pairs_per_s": st[2] / t_st, "bfs_levels": levels,
+                   "csr_entries_examined": examined, "teps": src.size * g.nnz / t_st,
+                   "algorithmic_bytes": st_bytes, "frac_of_hbm_peak": st_bytes / t_st / hbm},
+        "neighborhood_preservation": {
+            "value": npv[0], "queries": g.n, "ms": 1e3 * t_np, "distance_evals": evals,
+            "evals_per_s": evals / t_np, "frac_of_fp32_peak": evals / t_np / fp32_evals},
+    }
+
+
 def bench_attraction(lay, d_xy0, params, stream, flush, g, peaks):
     """Step a5 alone (bl_forces with BL_ATTRACTION_ONLY over all n vertices:
     the CSR attraction + neighbour correction of one whole iteration, edge-
@@ -581,6 +636,7 @@ def main(argv=None):
     ap.add_argument("--prof", action="store_true", help="add a phase profile (extra untimed run)")
     ap.add_argument("--no-bh", action="store_true", help="skip the secondary BatchLayoutBH line")
     ap.add_argument("--no-shuffle", action="store_true", help="skip the batch-randomisation object")
+    ap.add_argument("--no-metrics", action="store_true", help="skip the quality-metrics object")
     ap.add_argument("--theta", type=float, default=1.2, help="BatchLayoutBH MAC threshold (P:869)")
     ap.add_argument("--latency-configs", default="C2,C3b256,C4",
                     help="secondary latency-bound configs ('' to skip)")

@@ -12,6 +12,6 @@ from ._bl import (  # noqa: F401
     BLError, bl_params, bl_params_default, bl_greedy_init, bl_create, bl_layout, bl_layout_device,
     bl_energy, bl_forces, bl_max_vertices, bl_last_launch_count, bl_last_visits, bl_kernel_name, bl_driver_name, bl_edge_uniformity,
     bl_stress, bl_neighborhood_preservation, bl_microbench,
-    bl_destroy, bl_debug_profile, bl_debug_check, lib, _SO,
+    bl_destroy, bl_debug_profile, bl_debug_check, bl_debug_counters, lib, _SO,
 )
 from .layout import BatchLayout  # noqa: F401

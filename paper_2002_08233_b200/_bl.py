@@ -84,6 +84,8 @@ def _load() -> ctypes.CDLL:
     lib.bl_driver_name.restype = ctypes.c_char_p
     lib.bl_microbench.argtypes = [P(ctypes.c_double)]
     lib.bl_microbench.restype = ctypes.c_int
+    lib.bl_debug_counters.argtypes = [vp, vp]
+    lib.bl_debug_counters.restype = i32
     lib.bl_debug_check.argtypes = [vp, vp]
     lib.bl_debug_check.restype = i32
     lib.bl_debug_profile.argtypes = [vp, vp, i32]
@@ -103,7 +105,7 @@ lib = _load()
 EXPORTS = ("bl_params_default", "bl_greedy_init", "bl_create", "bl_layout", "bl_layout_device", "bl_energy",
            "bl_forces", "bl_max_vertices", "bl_last_launch_count", "bl_last_visits", "bl_kernel_name", "bl_driver_name", "bl_edge_uniformity",
            "bl_stress", "bl_neighborhood_preservation", "bl_microbench",
-           "bl_debug_profile", "bl_debug_check", "bl_destroy", "bl_status_string", "bl_last_error")
+           "bl_debug_profile", "bl_debug_check", "bl_debug_counters", "bl_destroy", "bl_status_string", "bl_last_error")
 
 
 def _check(rc: int, h=None):
@@ -256,6 +258,13 @@ def bl_microbench():
     _check(lib.bl_microbench(r))
     return {"ffma_per_clk_sm": r[0], "mufu_rcp_per_clk_sm": r[1], "mufu_rsq_per_clk_sm": r[2],
             "ffma2_lane_ops_per_clk_sm": r[3]}
+
+
+def bl_debug_counters(h: int):
+    """Work counters of the last bl_stress call: (BFS levels, CSR entries examined)."""
+    out = np.zeros(4, dtype=np.int64)
+    lib.bl_debug_counters(h, out.ctypes.data)
+    return int(out[0]), int(out[1])
 
 
 def bl_debug_check(h: int):

@@ -109,6 +109,14 @@ extern "C" int32_t bl_debug_check(bl_ctx *h, uint32_t *out) {
 #endif
 }
 
+// Work counters of the last bl_stress call on h (measurement aid): out[0] =
+// BFS levels summed over the 64-source groups, out[1] = CSR entries examined.
+extern "C" int32_t bl_debug_counters(const bl_ctx *h, int64_t *out) {
+  if (!h || !out) return -1;
+  for (int i = 0; i < 4; ++i) out[i] = h->m_counters[i];
+  return 4;
+}
+
 extern "C" const char *bl_kernel_name(const bl_ctx *h) {
   return h ? (h->kname_last[0] ? h->kname_last : h->kname) : "";
 }
@@ -333,6 +341,7 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_cellf);
   cudaFree(h->d_nleaf);
   cudaFree(h->d_leafv);
+  for (void *q : h->m_scr) cudaFree(q);
   cudaFree(h->d_chk);
   cudaFree(h->d_part_st);
   cudaFree(h->d_pend_st);

@@ -66,7 +66,11 @@ struct bl_ctx {
   // checked builds (-DBL_CHECKED): violation record and phase stamps
   unsigned *d_chk = nullptr, *d_part_st = nullptr, *d_pend_st = nullptr, *d_xy_st = nullptr;
   size_t part_st_cap = 0, pend_st_cap = 0;
-  // quality-metric scratch (allocated per call)
+  // quality-metric scratch: grown on first use, kept for the context's life
+  // (no allocation inside a metric call after the first)
+  void *m_scr[20] = {nullptr};
+  size_t m_cap[20] = {0};
+  long long m_counters[4] = {0, 0, 0, 0};  // bl_debug_counters
 };
 
 

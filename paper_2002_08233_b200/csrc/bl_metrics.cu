@@ -13,18 +13,36 @@
 // ------------------------------------------------------------------ metrics
 // Quality metrics of §3.7 (csrc/bl_metrics.cuh).  Synchronous on the stream.
 namespace {
+// context-owned scratch slot (bl_ctx::m_scr): a view that frees nothing
 struct DevBuf {
   void *p = nullptr;
-  ~DevBuf() { cudaFree(p); }
   template <typename T>
   T *as() { return reinterpret_cast<T *>(p); }
 };
+enum {
+  S_EU_PART, S_EU_STATS, S_ST_SRC, S_ST_VIS, S_ST_FA, S_ST_FB, S_ST_AA, S_ST_AB, S_ST_AN,
+  S_ST_FLAG, S_ST_BAR, S_ST_OUT4, S_ST_OUTN, S_NP_Q, S_NP_JAC, S_NP_OUT, S_NP_CNT, S_EU_ROW,
+  S_ST_WORK
+};
+cudaError_t scratch(bl_ctx *h, int slot, size_t bytes, DevBuf &buf) {
+  bytes = std::max<size_t>(bytes, 16);
+  if (h->m_cap[slot] < bytes) {
+    cudaFree(h->m_scr[slot]);
+    h->m_scr[slot] = nullptr;
+    h->m_cap[slot] = 0;
+    cudaError_t e = cudaMalloc(&h->m_scr[slot], bytes);
+    if (e != cudaSuccess) return e;
+    h->m_cap[slot] = bytes;
+  }
+  buf.p = h->m_scr[slot];
+  return cudaSuccess;
+}
 }  // namespace
 
-#define BLM_ALLOC(h, buf, bytes)                                                             \
+#define BLM_ALLOC(h, slot, buf, bytes)                                                        \
   do {                                                                                       \
-    cudaError_t e_ = cudaMalloc(&(buf).p, (bytes));                                          \
-    if (e_ != cudaSuccess) return bl_fail((h), BL_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e_)); \
+    cudaError_t e_ = scratch((h), (slot), (bytes), (buf));                                   \
+    if (e_ != cudaSuccess) return fail((h), BL_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e_)); \
   } while (0)
 
 extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu, void *cuda_stream) {
@@ -32,18 +50,26 @@ extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int nb = 4 * h->num_sms;
   DevBuf part, stats;
-  BLM_ALLOC(h, part, sizeof(double2) * nb);
-  BLM_ALLOC(h, stats, sizeof(double) * 8);
+  BLM_ALLOC(h, S_EU_PART, part, sizeof(double2) * nb);
+  BLM_ALLOC(h, S_EU_STATS, stats, sizeof(double) * 8);
   const float2 *xy = reinterpret_cast<const float2 *>(d_xy);
+  DevBuf row;
+  const bool fresh = h->m_cap[S_EU_ROW] == 0;
+  BLM_ALLOC(h, S_EU_ROW, row, sizeof(int) * std::max<size_t>(1, h->nnz));
+  int launches = 4;
+  if (fresh) {  // once per context: the COO row ids of the CSR entries
+    blm_coo_rows<<<nb, BLM_NT, 0, st>>>(h->d_rowptr, h->n, row.as<int>());
+    ++launches;
+  }
   for (int pass = 0; pass < 2; ++pass) {
-    blm_eu_pass<<<nb, BLM_NT, 0, st>>>(h->d_rowptr, h->d_colidx, xy, h->n, pass, stats.as<double>(),
-                                        part.as<double2>());
+    blm_eu_pass<<<nb, BLM_NT, 0, st>>>(row.as<int>(), h->d_colidx, xy, (long long)h->nnz, pass,
+                                        stats.as<double>(), part.as<double2>());
     blm_reduce_parts<<<1, 32, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
   }
   BL_CUDA(h, cudaGetLastError());
   BL_CUDA(h, cudaMemcpyAsync(eu, stats.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaStreamSynchronize(st));
-  h->launches = 4;
+  h->launches = launches;
   return BL_OK;
 }
 
@@ -66,17 +92,19 @@ extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sour
   BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blm_stress_kernel, BLM_NT, 0));
   const int G = h->num_sms * std::max(1, std::min(occ, 4));
   DevBuf d_src, vis, fa, fb, aA, aB, aN, flag, bar, out4, outN;
-  BLM_ALLOC(h, d_src, sizeof(int32_t) * nsrc);
-  BLM_ALLOC(h, vis, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, fa, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, fb, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, aA, sizeof(double) * G * BLM_NT);
-  BLM_ALLOC(h, aB, sizeof(double) * G * BLM_NT);
-  BLM_ALLOC(h, aN, sizeof(unsigned long long) * G * BLM_NT);
-  BLM_ALLOC(h, flag, sizeof(int) * 3);
-  BLM_ALLOC(h, bar, sizeof(unsigned));
-  BLM_ALLOC(h, out4, sizeof(double) * 4);
-  BLM_ALLOC(h, outN, sizeof(unsigned long long));
+  BLM_ALLOC(h, S_ST_SRC, d_src, sizeof(int32_t) * nsrc);
+  BLM_ALLOC(h, S_ST_VIS, vis, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, S_ST_FA, fa, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, S_ST_FB, fb, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, S_ST_AA, aA, sizeof(double) * G * BLM_NT);
+  BLM_ALLOC(h, S_ST_AB, aB, sizeof(double) * G * BLM_NT);
+  BLM_ALLOC(h, S_ST_AN, aN, sizeof(unsigned long long) * G * BLM_NT);
+  BLM_ALLOC(h, S_ST_FLAG, flag, sizeof(int) * 3);
+  BLM_ALLOC(h, S_ST_BAR, bar, sizeof(unsigned));
+  BLM_ALLOC(h, S_ST_OUT4, out4, sizeof(double) * 4);
+  BLM_ALLOC(h, S_ST_OUTN, outN, sizeof(unsigned long long) * 4);
+  DevBuf work;
+  BLM_ALLOC(h, S_ST_WORK, work, sizeof(unsigned long long) * ((size_t)G * BLM_NT + 1));
   BL_CUDA(h, cudaMemcpyAsync(d_src.p, src.data(), sizeof(int32_t) * nsrc, cudaMemcpyHostToDevice, st));
   BL_CUDA(h, cudaMemsetAsync(bar.p, 0, sizeof(unsigned), st));
   BLMStressParams k{};
@@ -94,16 +122,20 @@ extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sour
   k.accN = aN.as<unsigned long long>();
   k.flag = flag.as<int>();
   k.bar = bar.as<unsigned>();
+  k.work = work.as<unsigned long long>();
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel((void *)blm_stress_kernel, dim3(G), dim3(BLM_NT), args, 0, st));
-  blm_stress_reduce<<<1, 32, 0, st>>>(k.accA, k.accB, k.accN, G * BLM_NT, out4.as<double>(),
-                                      outN.as<unsigned long long>());
+  blm_stress_reduce<<<1, 32, 0, st>>>(k.accA, k.accB, k.accN, k.work, G * BLM_NT,
+                                      out4.as<double>(), outN.as<unsigned long long>());
   BL_CUDA(h, cudaGetLastError());
   double o[4];
-  unsigned long long N = 0;
+  unsigned long long NW[3] = {0, 0, 0};
   BL_CUDA(h, cudaMemcpyAsync(o, out4.p, sizeof o, cudaMemcpyDeviceToHost, st));
-  BL_CUDA(h, cudaMemcpyAsync(&N, outN.p, sizeof N, cudaMemcpyDeviceToHost, st));
+  BL_CUDA(h, cudaMemcpyAsync(NW, outN.p, sizeof NW, cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaStreamSynchronize(st));
+  const unsigned long long N = NW[0];
+  h->m_counters[0] = (long long)NW[2];
+  h->m_counters[1] = (long long)NW[1];
   *stress = o[0];
   if (scale) *scale = o[1];
   if (pairs) *pairs = (long long)N;
@@ -127,12 +159,12 @@ extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
   cudaStream_t st = (cudaStream_t)cuda_stream;
   DevBuf d_q, jac, out, cnt;
   if (queries) {
-    BLM_ALLOC(h, d_q, sizeof(int32_t) * nq);
+    BLM_ALLOC(h, S_NP_Q, d_q, sizeof(int32_t) * nq);
     BL_CUDA(h, cudaMemcpyAsync(d_q.p, queries, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st));
   }
-  BLM_ALLOC(h, jac, sizeof(double) * nq);
-  BLM_ALLOC(h, out, sizeof(double));
-  BLM_ALLOC(h, cnt, sizeof(int));
+  BLM_ALLOC(h, S_NP_JAC, jac, sizeof(double) * nq);
+  BLM_ALLOC(h, S_NP_OUT, out, sizeof(double));
+  BLM_ALLOC(h, S_NP_CNT, cnt, sizeof(int));
   blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx,
                                                 reinterpret_cast<const float2 *>(d_xy), n,
                                                 queries ? d_q.as<int>() : nullptr, nq, jac.as<double>());

@@ -36,41 +36,45 @@ __device__ __forceinline__ double blm_block_sum(double v, double *sh_warp) {
 }
 
 // ---------------------------------------------------------------- EU (M2)
+// COO row ids of the CSR entries (row[k] = i for rowptr[i] <= k < rowptr[i+1]),
+// built once per context on the first EU call: makes the EU passes purely
+// entry-parallel and coalesced whatever the degree skew.
+__global__ void blm_coo_rows(const int *rowptr, int n, int *row) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) row[k] = i;
+}
+
 // pass 0: part[b] = (sum of edge lengths, edge count); pass 1: part[b] =
-// sum (l - mu)^2 with mu = stats[0] / stats[1] from pass 0.
-// Edge-parallel: thread t owns the contiguous CSR entries [t*chunk, ...)
-// (balanced whatever the degree skew), finds its first row by binary search
-// over rowptr and walks on; fixed mapping -> deterministic sums.
-__global__ void __launch_bounds__(BLM_NT) blm_eu_pass(const int *rowptr, const int *colidx,
-                                                      const float2 *xy, int n, int pass,
+// sum (l - mu)^2 with mu = stats[0] / stats[1] from pass 0.  Each undirected
+// edge once (entries with j > i).  Entry-parallel, grid-stride with a fixed
+// grid: thread t takes entries t, t + T, t + 2T, ... (8 in flight), so every
+// per-thread sum has a fixed order -> bitwise-reproducible results.
+__global__ void __launch_bounds__(BLM_NT) blm_eu_pass(const int *row, const int *colidx,
+                                                      const float2 *xy, long long nnz, int pass,
                                                       const double *stats, double2 *part) {
   __shared__ double sh[BLM_NW];
   double acc = 0.0, cnt = 0.0;
   const double mu = pass ? stats[0] / stats[1] : 0.0;
-  const long long nnz = rowptr[n];
   const long long T = (long long)gridDim.x * BLM_NT;
-  const long long t = (long long)blockIdx.x * BLM_NT + threadIdx.x;
-  const long long chunk = (nnz + T - 1) / T;
-  const long long k0 = t * chunk, k1 = min(nnz, k0 + chunk);
-  if (k0 < k1) {
-    int lo = 0, hi = n - 1;  // largest i with rowptr[i] <= k0
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (rowptr[mid] <= k0) lo = mid;
-      else hi = mid - 1;
+  for (long long k0 = (long long)blockIdx.x * BLM_NT + threadIdx.x; k0 < nnz; k0 += 8 * T) {
+    int ii[8], jj[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long k = k0 + u * T;
+      ii[u] = k < nnz ? __ldg(row + k) : 0;
+      jj[u] = k < nnz ? __ldg(colidx + k) : 0;
     }
-    int i = lo, end_i = rowptr[i + 1];
-    float2 ci = xy[i];
-    for (long long k = k0; k < k1; ++k) {
-      while (k >= end_i) {
-        ++i;
-        end_i = rowptr[i + 1];
-        ci = xy[i];
-      }
-      const int j = colidx[k];
-      if (j <= i) continue;
-      const float2 cj = xy[j];
-      const double dx = (double)cj.x - (double)ci.x, dy = (double)cj.y - (double)ci.y;
+    float2 ci[8], cj[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool take = jj[u] > ii[u];
+      ci[u] = take ? __ldg(xy + ii[u]) : make_float2(0.f, 0.f);
+      cj[u] = take ? __ldg(xy + jj[u]) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (jj[u] <= ii[u]) continue;
+      const double dx = (double)cj[u].x - (double)ci[u].x, dy = (double)cj[u].y - (double)ci[u].y;
       const double l = sqrt(dx * dx + dy * dy);
       if (pass) {
         acc += (l - mu) * (l - mu);
@@ -114,6 +118,7 @@ struct BLMStressParams {
   unsigned long long *accN;
   int *flag;            // [3] per-level 'new pairs' flags, rotating
   unsigned *bar;
+  unsigned long long *work;  // [G * NT] CSR entries examined per thread; [G * NT] levels
 };
 
 __global__ void __launch_bounds__(BLM_NT, 1) blm_stress_kernel(BLMStressParams p) {
@@ -122,7 +127,7 @@ __global__ void __launch_bounds__(BLM_NT, 1) blm_stress_kernel(BLMStressParams p
   const int G = gridDim.x, tid = blockIdx.x * BLM_NT + threadIdx.x, GT = G * BLM_NT;
   unsigned bar_target = 0;
   double A = 0.0, B = 0.0;
-  unsigned long long N = 0;
+  unsigned long long N = 0, examined = 0, levels = 0;
   for (int g0 = 0; g0 < p.nsrc; g0 += 64) {
     const int gs = min(64, p.nsrc - g0);
     // init the group: no vertex visited except the sources
@@ -147,7 +152,9 @@ __global__ void __launch_bounds__(BLM_NT, 1) blm_stress_kernel(BLMStressParams p
         unsigned long long nb = 0ull;
         if (vv != full) {
           unsigned long long acc = 0ull;
-          for (int k = p.rowptr[v]; k < p.rowptr[v + 1]; ++k) acc |= __ldcg(cur + p.colidx[k]);
+          const int k0 = p.rowptr[v], k1 = p.rowptr[v + 1];
+          for (int k = k0; k < k1; ++k) acc |= __ldcg(cur + p.colidx[k]);
+          examined += (unsigned long long)(k1 - k0);
           nb = acc & ~vv;
         }
         nxt[v] = nb;
@@ -171,6 +178,7 @@ __global__ void __launch_bounds__(BLM_NT, 1) blm_stress_kernel(BLMStressParams p
       }
       // slot (L+1)%3 was last read after barrier L-2: everyone is past it
       if (tid == 0) p.flag[(L + 1) % 3] = 0;
+      ++levels;
       bl_grid_sync(p.bar, bar_target, &unit_dummy);
       const int more = __ldcg(p.flag + (L % 3));
       unsigned long long *t = cur;
@@ -183,21 +191,26 @@ __global__ void __launch_bounds__(BLM_NT, 1) blm_stress_kernel(BLMStressParams p
   p.accA[tid] = A;
   p.accB[tid] = B;
   p.accN[tid] = N;
+  p.work[tid] = examined;
+  if (tid == 0) p.work[GT] = levels;
 }
 
 // final fixed-order sums of the per-thread partials and the closed form of
 // the scale-optimised stress (M1): out4 = (ST, s*, A, B), outN = pairs
 __global__ void blm_stress_reduce(const double *accA, const double *accB,
-                                  const unsigned long long *accN, int count, double *out4,
-                                  unsigned long long *outN) {
+                                  const unsigned long long *accN, const unsigned long long *work,
+                                  int count, double *out4, unsigned long long *outN) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double A = 0.0, B = 0.0;
-    unsigned long long N = 0;
+    unsigned long long N = 0, W = 0;
     for (int t = 0; t < count; ++t) {
       A += accA[t];
       B += accB[t];
       N += accN[t];
+      W += work[t];
     }
+    outN[1] = W;            // CSR entries examined (all groups, all levels)
+    outN[2] = work[count];  // BFS levels (all groups)
     const double sc = B > 0.0 ? A / B : 0.0;
     out4[0] = sc * sc * B - 2.0 * sc * A + (double)N;
     out4[1] = sc;
