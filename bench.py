@@ -589,9 +589,11 @@ def bench_attraction(lay, d_xy0, params, stream, flush, g, peaks):
                      "frac_of_hbm_peak": nbytes / t / 1e9 / float(peaks.get("hbm_gbs", 6540.2))}
     out.update({"step": "a5 (CSR attraction + neighbour correction), all n vertices, one launch",
                 "algorithmic_bytes": nbytes, "csr_entries": int(g.nnz),
-                "kernel": bl.bl_kernel_name(lay.h) + " (forces mode, attraction only)",
-                "note": "latency-bound gathers (12 B per entry); in the layout the same code "
-                        "runs inside the update tasks, overlapped with the sweep"})
+                "kernel": bl.bl_kernel_name(lay.h),
+                "gpu_launches": bl.bl_last_launch_count(lay.h),
+                "note": "standalone high-occupancy kernels (bl_attr.cuh, 64 warps/SM, 8 gathers "
+                        "in flight per lane); in the layout the same arithmetic runs inside the "
+                        "update tasks, overlapped with the sweep"})
     return out
 
 

@@ -465,6 +465,17 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.f_out = f_out;
   k.prof = h->d_prof;
 
+  if (attr_only) {
+    // step a5 alone: the standalone high-occupancy kernels (bl_attr.cuh)
+    model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
+    cudaError_t e = bl_attr_launch(k, st, h->item_ptr[first], h->item_ptr[first + count],
+                                   h->num_sms);
+    if (e != cudaSuccess) return bl_fail(h, BL_ECUDA, "attraction kernels: %s", cudaGetErrorString(e));
+    snprintf(h->kname_last, sizeof h->kname_last, "bla_items_kernel + bla_sum_kernel");
+    h->driver_last = "standalone";
+    h->launches = 2;
+    return BL_OK;
+  }
   k.red_cap = red_cap_for(k.chunk4);
   k.guided = env_int("BL_GUIDED", 2);
   k.min_unit4 = std::max(1, env_int("BL_MIN_UNIT4", BL_MIN_UNIT4));

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -96,3 +97,5 @@ void *bl_bh_kernel_fn();                            // bl_bh.cu
 size_t bl_bh_smem_bytes();
 int bl_bh_threads();
 void *bl_cluster_kernel_fn(int tt, int rmode);      // bl_cluster.cu
+// bl_attr.cu: step a5 alone (bl_forces + BL_ATTRACTION_ONLY), two launches
+cudaError_t bl_attr_launch(const BLKParams &k, cudaStream_t st, int ib, int ie, int num_sms);
