@@ -6,5 +6,6 @@
 extern const BLVariant bl_exact_v0[] = {
     {512, 8, 2, (void *)bl_layout_kernel<512, 8, 2>},
     {512, 8, -1, (void *)bl_layout_kernel<512, 8, -1>},
+    {512, 8, 1, (void *)bl_layout_kernel<512, 8, 1>},
 };
-extern const int bl_exact_v0_count = 2;
+extern const int bl_exact_v0_count = 3;
