@@ -84,10 +84,13 @@ def _load() -> ctypes.CDLL:
     lib.bl_driver_name.restype = ctypes.c_char_p
     lib.bl_microbench.argtypes = [P(ctypes.c_double)]
     lib.bl_microbench.restype = ctypes.c_int
-    lib.bl_debug_counters.argtypes = [vp, vp]
-    lib.bl_debug_counters.restype = i32
-    lib.bl_debug_check.argtypes = [vp, vp]
-    lib.bl_debug_check.restype = i32
+    # debug aids: absent from older builds loaded through BL_LIBRARY (A/B runs)
+    if hasattr(lib, "bl_debug_counters"):
+        lib.bl_debug_counters.argtypes = [vp, vp]
+        lib.bl_debug_counters.restype = i32
+    if hasattr(lib, "bl_debug_check"):
+        lib.bl_debug_check.argtypes = [vp, vp]
+        lib.bl_debug_check.restype = i32
     lib.bl_debug_profile.argtypes = [vp, vp, i32]
     lib.bl_debug_profile.restype = i32
     lib.bl_destroy.argtypes = [vp]
