@@ -238,10 +238,13 @@ int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t len);
  * recorded, out zeroed) or -1 (NULL argument / CUDA error). */
 int32_t bl_debug_check(bl_ctx *h, uint32_t *out);
 
-/* Measurement aid: work counters of the last bl_stress call on h -- out[0] =
- * BFS levels summed over its 64-source groups, out[1] = CSR entries examined
- * (each level pulls the rows of the not-yet-complete vertices); out[2..3] = 0.
- * Returns 4, or -1 on a NULL argument. */
+/* Measurement aid: out[0] = BFS levels summed over the 64-source groups and
+ * out[1] = CSR entries examined (each level pulls the rows of the
+ * not-yet-complete vertices) by the last bl_stress call on h; out[2] = GPU
+ * time in ns of the kernels of the last metric call (bl_edge_uniformity,
+ * bl_stress or bl_neighborhood_preservation; CUDA events on its stream, no
+ * host synchronisation included); out[3] = 0.  Returns 4, or -1 on a NULL
+ * argument. */
 int32_t bl_debug_counters(const bl_ctx *h, int64_t *out);
 
 void bl_destroy(bl_ctx *h);

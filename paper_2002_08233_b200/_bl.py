@@ -264,10 +264,11 @@ def bl_microbench():
 
 
 def bl_debug_counters(h: int):
-    """Work counters of the last bl_stress call: (BFS levels, CSR entries examined)."""
+    """(BFS levels, CSR entries examined) of the last bl_stress call, GPU ns of
+    the last metric call's kernels."""
     out = np.zeros(4, dtype=np.int64)
     lib.bl_debug_counters(h, out.ctypes.data)
-    return int(out[0]), int(out[1])
+    return int(out[0]), int(out[1]), int(out[2])
 
 
 def bl_debug_check(h: int):

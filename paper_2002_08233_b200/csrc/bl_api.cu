@@ -109,8 +109,9 @@ extern "C" int32_t bl_debug_check(bl_ctx *h, uint32_t *out) {
 #endif
 }
 
-// Work counters of the last bl_stress call on h (measurement aid): out[0] =
-// BFS levels summed over the 64-source groups, out[1] = CSR entries examined.
+// Work counters (measurement aid): out[0] = BFS levels summed over the
+// 64-source groups and out[1] = CSR entries examined by the last bl_stress
+// call; out[2] = GPU time (ns) of the last metric call's kernels.
 extern "C" int32_t bl_debug_counters(const bl_ctx *h, int64_t *out) {
   if (!h || !out) return -1;
   for (int i = 0; i < 4; ++i) out[i] = h->m_counters[i];
@@ -125,7 +126,7 @@ extern "C" const char *bl_kernel_name(const bl_ctx *h) {
 // context was created with BL_PROFILE=1 (bench.py --prof).
 extern "C" int32_t bl_debug_profile(bl_ctx *h, unsigned long long *out, int32_t len) {
   if (!h || !h->d_prof || !out) return 0;
-  const int m = std::min<int>(len, 8 + h->G);
+  const int m = std::min<int>(len, 16 + h->G);
   if (cudaMemcpy(out, h->d_prof, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
   return m;
@@ -297,7 +298,7 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   const int per_sm = std::max(1, env_int("BL_CTAS_PER_SM", 1));
   h->G = h->num_sms * per_sm;
   h->prof = env_int("BL_PROFILE", 0) != 0;
-  if (h->prof && cudaMalloc((void **)&h->d_prof, sizeof(unsigned long long) * (8 + h->G)) != cudaSuccess)
+  if (h->prof && cudaMalloc((void **)&h->d_prof, sizeof(unsigned long long) * (16 + h->G)) != cudaSuccess)
     return bad(bl_fail(h, BL_ENOMEM, "profile buffer"));
   *out = h;
   return BL_OK;
@@ -342,6 +343,8 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_nleaf);
   cudaFree(h->d_leafv);
   for (void *q : h->m_scr) cudaFree(q);
+  for (cudaEvent_t e : h->m_ev)
+    if (e) cudaEventDestroy(e);
   cudaFree(h->d_chk);
   cudaFree(h->d_part_st);
   cudaFree(h->d_pend_st);
@@ -447,6 +450,23 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // one barrier per batch needs >= 4 batches per iteration,
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
+  // kernel variant: r != -1 -> <512,8,-1> (two MUFU per pair);
+  // very large batches (b n >= 5e8, e.g. 2^20 vertices x 1024) -> <256,16,6>
+  // (fewer, wider warps amortise best); latency-bound batches (b n <=
+  // BL_SMALL_PAIRS, default 2^24) -> <512,2,1>: 64-target tiles and >= 4-slot
+  // sub-ranges spread each batch's small sweep over all 16 warps instead of
+  // a few long units (measured: C2 -17 %, C3 b=256 -29 %, C4 -23 % per batch
+  // vs <512,8,2>); else <512,8,2>.  BL_NT / BL_T / BL_TP (read at bl_create)
+  // pin a variant.
+  model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
+  const long long bn = (long long)b * n;
+  const bool user_variant = getenv("BL_NT") || getenv("BL_T") || getenv("BL_TP");
+  const bool wide = !user_variant && bn >= 500000000LL;
+  const bool small_b = !user_variant && bn <= (long long)env_int("BL_SMALL_PAIRS", 1 << 24);
+  const BLVariant *vt = k.rmode != 0 ? find_variant(512, 8, -1)
+                        : wide && !attr_only ? find_variant(256, 16, 6)
+                        : small_b && !attr_only ? find_variant(512, 2, 1)
+                                              : find_variant(h->NT, h->T, h->TP);
   // batch randomisation (readings R1-R2): the two-barrier driver (its phase U
   // takes batch positions, not owned vertices)
   k.shuf_seed = forces_mode ? 0ull : (unsigned long long)p->shuffle_seed;
@@ -454,7 +474,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   while ((1LL << (2 * k.shuf_h)) < (long long)n) ++k.shuf_h;
   k.pipelined = !forces_mode && k.shuf_seed == 0 && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
                 (b + G - 1) / G <= BL_ETASK_MAX &&
-                red_cap_for(chunk4_for(n, G)) / (((b + 32 * h->T - 1) / (32 * h->T)) * 32 * h->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
+                red_cap_for(chunk4_for(n, G)) / (((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T) >= 2 && (((uintptr_t)d_xy) & 15) == 0 &&
                 env_int("BL_PIPELINE", 1) != 0;
   k.part_nbuf = 2;
   k.attr = h->d_attr;
@@ -478,23 +498,17 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   }
   k.red_cap = red_cap_for(k.chunk4);
   k.guided = env_int("BL_GUIDED", 2);
-  k.min_unit4 = std::max(1, env_int("BL_MIN_UNIT4", BL_MIN_UNIT4));
-  model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
-  // very large batches (b n >= 5e8 pairs, e.g. 2^20 vertices x 1024) amortise
-  // the fewer, wider warps of <256,16,6> best; below, <512,8,2> (measured)
-  const bool wide = !getenv("BL_NT") && (long long)b * n >= 500000000LL;
-  const BLVariant *vt = k.rmode != 0 ? find_variant(512, 8, -1)
-                        : wide && !attr_only ? find_variant(256, 16, 6)
-                                     : find_variant(h->NT, h->T, h->TP);
+  k.min_unit4 = std::max(1, env_int("BL_MIN_UNIT4", small_b ? 4 : BL_MIN_UNIT4));
   void *kfn = vt->fn;
   // asynchronous phases (bl_run_async) when each half of the partial buffer
   // still holds >= 2 sub-ranges of the batch's target tiles, and the batch's
-  // pair work is not tiny (measured with the tuned driver, same box: C5,
-  // b n = 2.7e8, +13 %; C3 b=1024, 1.1e7, +10 %; C4, 8.4e6, +2 %; C3 b=256,
-  // 2.8e6, -16 %; C2, 1.5e6, -22 %: latency-bound batches keep the pipelined
-  // driver).  BL_ASYNC=1 / 0 forces it on / off.
+  // pair work is not tiny with wide tiles (measured, same box, round 1 with
+  // <512,8,2>: C5 +13 %, C3 b=1024 +10 %, C4 +2 %, C3 b=256 -16 %, C2 -22 %;
+  // round 2 with the <512,2,1> small-batch variant, async beats pipelined
+  // everywhere: C2 6.6 vs 7.4 us, C3 b=256 6.5 vs 7.4, C4 8.8 vs 10.1 per
+  // batch).  BL_ASYNC=1 / 0 forces it on / off.
   const int async_env = env_int("BL_ASYNC", -1);
-  const bool async_auto = (long long)b * n >= (1LL << 22);
+  const bool async_auto = vt->T <= 2 || bn >= (1LL << 22);
   if (k.pipelined && (async_env == 1 || (async_env < 0 && async_auto)) &&
       (b + 32 * vt->T - 1) / (32 * vt->T) <= BL_NTT_MAX &&
       k.red_cap / 2 / (((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T) >= 2) {
@@ -550,7 +564,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // forces mode never writes iters_done: leave the last layout call's count
   // (and its energy trace) to bl_energy
   if (!forces_mode) BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
-  if (h->d_prof) BL_CUDA(h, cudaMemsetAsync(h->d_prof, 0, sizeof(unsigned long long) * (8 + G), st));
+  if (h->d_prof) BL_CUDA(h, cudaMemsetAsync(h->d_prof, 0, sizeof(unsigned long long) * (16 + G), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(vt->NT), args, smem, st));
   h->launches = 1;

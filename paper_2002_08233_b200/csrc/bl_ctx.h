@@ -72,6 +72,7 @@ struct bl_ctx {
   void *m_scr[20] = {nullptr};
   size_t m_cap[20] = {0};
   long long m_counters[4] = {0, 0, 0, 0};  // bl_debug_counters
+  cudaEvent_t m_ev[2] = {nullptr, nullptr};  // GPU time of the last metric call
 };
 
 

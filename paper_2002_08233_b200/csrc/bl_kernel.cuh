@@ -371,6 +371,15 @@ __device__ __forceinline__ float bl_model_coef(const P &p, float d2, float rs, f
   return fmaf(rep, rv, at * p.invK);
 }
 
+// CTA-scope release/acquire fence for the task-queue handshakes in shared
+// memory (a flag written after data / read before data): fence.acq_rel.cta,
+// not the sequentially consistent MEMBAR.SC.CTA of __threadfence_block().
+__device__ __forceinline__ void bl_fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+__device__ __forceinline__ unsigned bl_ld_relaxed(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned bl_ld_acquire(const unsigned *p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -902,6 +911,7 @@ struct BLShared {
   // at C5 even when disabled at run time, so they are compiled out by
   // default): phase start, control claimed / published, last update done
   long long ts_start, ts_claim, ts_ready, ts_upd;
+  long long ts_upd_a, ts_arr_prev;  // async driver: updates done, previous arrival
 #endif
 };
 
@@ -1157,7 +1167,7 @@ __device__ __forceinline__ void bl_stage_rows_warp(const BLKParams &p, int q, BL
 // GPU fence).  BL_AFENCE=1 (debug) fences at GPU scope in every task instead.
 __device__ __forceinline__ void bl_fence_to_completer(const BLKParams &p) {
   if (p.afence_gpu) __threadfence();
-  else __threadfence_block();
+  else bl_fence_cta();
 }
 
 __device__ __forceinline__ void bl_token(const BLKParams &p, BLShared &sh, const BLPhase &f,
@@ -1167,7 +1177,7 @@ __device__ __forceinline__ void bl_token(const BLKParams &p, BLShared &sh, const
   const int tok = atomicAdd(&sh.a_tok[f.ph & 1], 1);
   BL_CHK(tok < need, BLC_TOKENS, f.ph, tok);
   if (tok != need - 1) return;
-  __threadfence_block();
+  bl_fence_cta();
   const int G = gridDim.x, c = blockIdx.x;
   if (f.owned > 0) {
     double e = sh.e_acc;
@@ -1178,9 +1188,33 @@ __device__ __forceinline__ void bl_token(const BLKParams &p, BLShared &sh, const
     p.e_cta[((f.q1 / p.nb) & 1) * G + c] = sh.e_acc;
     sh.e_acc = 0.0;
   }
+#ifdef BL_PHASE_TS
+  const long long t_tok = clock64();
+#endif
   if (f.ph <= f.P)
     asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar)
                  : "memory");
+#ifdef BL_PHASE_TS
+  // async critical-path timeline of CTA 0: per phase, barrier
+  // ph-1 + its detection, control, updates, tail (dirty units + tile
+  // combines after the later of control and updates), arrival
+  if (p.prof && c == 0) {
+    const long long t_arr = clock64();
+    unsigned long long *hp = p.prof + 8 + G;
+    if (f.ph > 0) {
+      long long last = sh.ts_ready > sh.ts_claim ? sh.ts_ready : sh.ts_claim;
+      if (f.owned > 0 && sh.ts_upd_a > last) last = sh.ts_upd_a;
+      hp[0] += (unsigned long long)(sh.ts_claim - sh.ts_arr_prev);
+      hp[1] += (unsigned long long)(sh.ts_ready - sh.ts_claim);
+      if (f.owned > 0) hp[2] += (unsigned long long)(sh.ts_upd_a - sh.ts_claim);
+      hp[3] += (unsigned long long)(t_tok > last ? t_tok - last : 0);
+      hp[4] += (unsigned long long)(t_arr - t_tok);
+      hp[5] += 1ull;
+      if (f.owned > 0) hp[6] += 1ull;
+    }
+    sh.ts_arr_prev = t_arr;
+  }
+#endif
 }
 
 // Control work of phase ph, attempted by a warp between tasks: if barrier
@@ -1190,14 +1224,18 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
                                                unsigned bar_target, int need = -1) {
   const int lane = threadIdx.x & 31;
   int go = 0;
-  if (lane == 0 && ((int)(bl_ld_acquire(p.bar) - bar_target) >= 0 || (BL_CHK_ON && p.chk_break)))
+  // poll with a relaxed load (an acquire load costs an L1 invalidation per
+  // poll); the claimant alone then acquires with a GPU-scope fence
+  if (lane == 0 && ((int)(bl_ld_relaxed(p.bar) - bar_target) >= 0 || (BL_CHK_ON && p.chk_break))) {
     go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
+    if (go) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
 #ifdef BL_PHASE_TS
   if (go && p.prof) sh.ts_claim = clock64();
 #endif
   if (go) {
     *(volatile int *)&sh.seen = f.ph;  // release the update tasks now
-    __threadfence_block();
+    bl_fence_cta();
   }
   go = __shfl_sync(0xffffffffu, go, 0);
   if (!go) return false;
@@ -1250,7 +1288,7 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
   __syncwarp();
   if (lane == 0) {
     if (stop) *(volatile int *)&sh.stop_flag = 1;
-    __threadfence_block();
+    bl_fence_cta();
 #ifdef BL_PHASE_TS
     if (p.prof) sh.ts_ready = clock64();
 #endif
@@ -1270,7 +1308,7 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
   if (lane == 0) t = atomicAdd(&sh.u_next, 1);
   t = __shfl_sync(0xffffffffu, t, 0);
   if (t >= f.owned) return false;
-  __threadfence_block();  // acquire the control warp's publication
+  bl_fence_cta();  // acquire the control warp's publication
   const int buf = f.q1 & 1;
   const volatile BLShared &vsh = sh;
   const bool staged = vsh.rowq[buf] == f.q1 && vsh.rdeg[buf][t] >= 0;
@@ -1282,7 +1320,7 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
 #ifdef BL_CHECKED
     sh.chk_upd[t] = f.q1 + 1;
 #endif
-    __threadfence_block();
+    bl_fence_cta();
 #ifdef BL_PHASE_TS
     if (atomicAdd(&sh.u_done, 1) == f.owned - 1 && p.prof) sh.ts_upd = clock64();
 #else
@@ -1326,7 +1364,7 @@ __device__ __forceinline__ void bl_phase_tasks(const BLKParams &p, const BLPhase
           if ((f.ph == 0 || vs.seen == f.ph) && (vs.stop_flag || vs.u_done >= f.owned)) break;
           __nanosleep(64);
         }
-        __threadfence_block();
+        bl_fence_cta();
 #ifdef BL_CHECKED
         if (!vs.stop_flag)
           for (int t = 0; t < f.owned; ++t)
@@ -1463,7 +1501,7 @@ __device__ __forceinline__ bool bl_try_update_a(const BLKParams &p, const BLPhas
   if (lane == 0) t = atomicAdd(&sh.a_unext[s], 1);
   t = __shfl_sync(0xffffffffu, t, 0);
   if (t >= f.owned) return false;
-  __threadfence_block();  // acquire the control warp's publication
+  bl_fence_cta();  // acquire the control warp's publication
   const int buf = f.q1 & 1;
   const bool staged = vs.rowq[buf] == f.q1 && vs.rdeg[buf][t] >= 0;
   bl_jitter(p, 22);
@@ -1477,7 +1515,10 @@ __device__ __forceinline__ bool bl_try_update_a(const BLKParams &p, const BLPhas
     bl_jitter(p, 23);
     bl_fence_to_completer(p);  // pend (read by other CTAs after barrier ph)
     if (atomicAdd(&sh.a_udone[s], 1) == f.owned - 1) {
-      __threadfence_block();
+#ifdef BL_PHASE_TS
+      sh.ts_upd_a = clock64();
+#endif
+      bl_fence_cta();
       *(volatile int *)&sh.a_updph = f.ph;
     }
     bl_token(p, sh, f, need);
@@ -1571,7 +1612,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
       gate_ns = 32;
       BL_WT(0);
       if (stop) break;
-      __threadfence_block();
+      bl_fence_cta();
       BL_CHK(vs.a_gen[s] == ph, BLC_SLOT_GEN, ph, vs.a_gen[s]);
     }
     prev_owned = f.owned;
@@ -1637,7 +1678,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
           }
           BL_WT(2);
           if (stop) break;
-          __threadfence_block();
+          bl_fence_cta();
 #ifdef BL_CHECKED
           for (int t = 0; t < f.owned; ++t)
             BL_CHK(((volatile int *)sh.chk_upd)[t] == f.q1 + 1, BLC_DIRTY_EARLY, ph, t);
@@ -1651,12 +1692,12 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
         __syncwarp();
         int last = 0;
         if (lane == 0) {
-          __threadfence_block();
+          bl_fence_cta();
           last = atomicAdd(&sh.a_tdone[s][tile], 1) == U.nsub - 1;
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
-          __threadfence_block();
+          bl_fence_cta();
           if (U.nsub > 1) {
             const int stride = U.ntt * 32 * T;
 #pragma unroll
@@ -1696,11 +1737,11 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
     if (stop) break;
     // leave the phase; the last warp out releases slot s for phase ph+2
     if (lane == 0 && atomicAdd(&sh.a_exit[s], 1) == BL_NW - 1) {
-      __threadfence_block();
+      bl_fence_cta();
       sh.a_unit[s] = sh.a_tok[s] = sh.a_unext[s] = sh.a_udone[s] = 0;
       for (int t = 0; t < BL_NTT_MAX; ++t) sh.a_tdone[s][t] = 0;
       sh.a_exit[s] = 0;
-      __threadfence_block();
+      bl_fence_cta();
       *(volatile int *)&sh.a_gen[s] = ph + 2;
     }
     __syncwarp();

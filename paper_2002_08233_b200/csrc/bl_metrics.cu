@@ -37,6 +37,19 @@ cudaError_t scratch(bl_ctx *h, int slot, size_t bytes, DevBuf &buf) {
   buf.p = h->m_scr[slot];
   return cudaSuccess;
 }
+// events around a metric call's kernels: their GPU time -> m_counters[2]
+cudaError_t mark(bl_ctx *h, int k, cudaStream_t st) {
+  if (!h->m_ev[k]) {
+    cudaError_t e = cudaEventCreate(&h->m_ev[k]);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaEventRecord(h->m_ev[k], st);
+}
+void record_time(bl_ctx *h) {
+  float ms = 0.f;
+  if (h->m_ev[0] && h->m_ev[1] && cudaEventElapsedTime(&ms, h->m_ev[0], h->m_ev[1]) == cudaSuccess)
+    h->m_counters[2] = (long long)(ms * 1e6);
+}
 }  // namespace
 
 #define BLM_ALLOC(h, slot, buf, bytes)                                                        \
@@ -57,6 +70,7 @@ extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu
   const bool fresh = h->m_cap[S_EU_ROW] == 0;
   BLM_ALLOC(h, S_EU_ROW, row, sizeof(int) * std::max<size_t>(1, h->nnz));
   int launches = 4;
+  BL_CUDA(h, mark(h, 0, st));
   if (fresh) {  // once per context: the COO row ids of the CSR entries
     blm_coo_rows<<<nb, BLM_NT, 0, st>>>(h->d_rowptr, h->n, row.as<int>());
     ++launches;
@@ -67,8 +81,10 @@ extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu
     blm_reduce_parts<<<1, 32, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
   }
   BL_CUDA(h, cudaGetLastError());
+  BL_CUDA(h, mark(h, 1, st));
   BL_CUDA(h, cudaMemcpyAsync(eu, stats.as<double>() + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaStreamSynchronize(st));
+  record_time(h);
   h->launches = launches;
   return BL_OK;
 }
@@ -124,16 +140,19 @@ extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sour
   k.bar = bar.as<unsigned>();
   k.work = work.as<unsigned long long>();
   void *args[] = {&k};
+  BL_CUDA(h, mark(h, 0, st));
   BL_CUDA(h, cudaLaunchCooperativeKernel((void *)blm_stress_kernel, dim3(G), dim3(BLM_NT), args, 0, st));
   blm_stress_reduce<<<1, 32, 0, st>>>(k.accA, k.accB, k.accN, k.work, G * BLM_NT,
                                       out4.as<double>(), outN.as<unsigned long long>());
   BL_CUDA(h, cudaGetLastError());
+  BL_CUDA(h, mark(h, 1, st));
   double o[4];
   unsigned long long NW[3] = {0, 0, 0};
   BL_CUDA(h, cudaMemcpyAsync(o, out4.p, sizeof o, cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaMemcpyAsync(NW, outN.p, sizeof NW, cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaStreamSynchronize(st));
   const unsigned long long N = NW[0];
+  record_time(h);
   h->m_counters[0] = (long long)NW[2];
   h->m_counters[1] = (long long)NW[1];
   *stress = o[0];
@@ -165,16 +184,19 @@ extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
   BLM_ALLOC(h, S_NP_JAC, jac, sizeof(double) * nq);
   BLM_ALLOC(h, S_NP_OUT, out, sizeof(double));
   BLM_ALLOC(h, S_NP_CNT, cnt, sizeof(int));
+  BL_CUDA(h, mark(h, 0, st));
   blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx,
                                                 reinterpret_cast<const float2 *>(d_xy), n,
                                                 queries ? d_q.as<int>() : nullptr, nq, jac.as<double>());
   blm_np_reduce<<<1, 32, 0, st>>>(jac.as<double>(), nq, out.as<double>(), cnt.as<int>());
   BL_CUDA(h, cudaGetLastError());
+  BL_CUDA(h, mark(h, 1, st));
   int c = 0;
   BL_CUDA(h, cudaMemcpyAsync(np, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaMemcpyAsync(&c, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   BL_CUDA(h, cudaStreamSynchronize(st));
   if (counted) *counted = c;
+  record_time(h);
   h->launches = 2;
   return BL_OK;
 }

@@ -20,6 +20,7 @@ from blgen import build_config  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--mhz", type=float, default=1965.0, help="SM clock for cycles -> us")
 a = ap.parse_args()
 g, xy0, cfg = build_config(a.config)
 names = ["entry_gate", "idle", "dirty_wait", "units", "tile_combine", "updates", "control"]
@@ -32,7 +33,7 @@ with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
                       cooling=cfg.cooling)
     en.record()
     torch.cuda.synchronize()
-    pr = bl.bl_debug_profile(lay.h).astype(float)
+    pr = bl.bl_debug_profile(lay.h, 16 + 1024).astype(float)
     tot = pr[7]
     out = {"config": a.config, "iters": a.iters, "driver": bl.bl_driver_name(lay.h),
            "kernel": bl.bl_kernel_name(lay.h), "ms": st.elapsed_time(en),
@@ -43,4 +44,15 @@ with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
                            "std": float(busy.std()),
                            "slowest_ctas": [int(i) for i in busy.argsort()[-8:][::-1]],
                            "fastest_ctas": [int(i) for i in busy.argsort()[:8]]}
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    hp = pr[8 + G:8 + G + 8]
+    mhz = float(a.mhz)
+    if hp.size >= 7 and hp[5] > 0:
+        nph, nown = hp[5], max(hp[6], 1.0)
+        out["cta0_timeline_us_per_batch"] = {
+            "barrier_and_detection": hp[0] / nph / mhz, "control": hp[1] / nph / mhz,
+            "updates_after_claim": hp[2] / nown / mhz, "tail_dirty_and_tiles": hp[3] / nph / mhz,
+            "arrival_fence_red": hp[4] / nph / mhz, "phases": int(nph),
+            "phases_with_updates": int(hp[6]),
+            "total_batch_us": out["ms"] * 1e3 / (a.iters * -(-g.n // cfg.batch))}
     print(json.dumps(out, indent=1))
