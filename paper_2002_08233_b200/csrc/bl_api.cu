@@ -238,6 +238,7 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   if (!h) return bl_fail(nullptr, BL_ENOMEM, "host allocation failed");
   h->n = n;
   h->nnz = nnz;
+  h->rowptr_host.assign(rowptr, rowptr + (size_t)n + 1);
   auto bad = [&](bl_status s) {
     g_create_err = h->err;
     bl_destroy(h);
@@ -345,6 +346,8 @@ extern "C" void bl_destroy(bl_ctx *h) {
   for (void *q : h->m_scr) cudaFree(q);
   for (cudaEvent_t e : h->m_ev)
     if (e) cudaEventDestroy(e);
+  cudaFree(h->d_coo_row);
+  cudaFree(h->d_apart);
   cudaFree(h->d_chk);
   cudaFree(h->d_part_st);
   cudaFree(h->d_pend_st);
@@ -488,10 +491,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   if (attr_only) {
     // step a5 alone: the standalone high-occupancy kernels (bl_attr.cuh)
     model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
-    cudaError_t e = bl_attr_launch(k, st, h->item_ptr[first], h->item_ptr[first + count],
-                                   h->num_sms);
-    if (e != cudaSuccess) return bl_fail(h, BL_ECUDA, "attraction kernels: %s", cudaGetErrorString(e));
-    snprintf(h->kname_last, sizeof h->kname_last, "bla_items_kernel + bla_sum_kernel");
+    if ((s = bl_attr_launch(h, k, st)) != BL_OK) return s;
+    snprintf(h->kname_last, sizeof h->kname_last, "bla_edge_kernel + bla_row_sum_kernel");
     h->driver_last = "standalone";
     h->launches = 2;
     return BL_OK;

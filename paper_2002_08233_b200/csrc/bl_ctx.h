@@ -21,6 +21,9 @@ struct bl_ctx {
   int *d_rowptr = nullptr, *d_colidx = nullptr;
   int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
   std::vector<int> item_ptr;  // host copy (per-batch maxima)
+  std::vector<int> rowptr_host;  // host copy of rowptr (entry ranges)
+  int *d_coo_row = nullptr;      // COO row id per CSR entry (a5 alone, EU)
+  float2 *d_apart = nullptr;     // a5 alone: one partial per (lane, row) segment
   int n_items = 0;
   // scratch
   float2 *d_part = nullptr;
@@ -98,5 +101,7 @@ void *bl_bh_kernel_fn();                            // bl_bh.cu
 size_t bl_bh_smem_bytes();
 int bl_bh_threads();
 void *bl_cluster_kernel_fn(int tt, int rmode);      // bl_cluster.cu
-// bl_attr.cu: step a5 alone (bl_forces + BL_ATTRACTION_ONLY), two launches
-cudaError_t bl_attr_launch(const BLKParams &k, cudaStream_t st, int ib, int ie, int num_sms);
+// bl_attr.cu: step a5 alone (bl_forces + BL_ATTRACTION_ONLY), two launches;
+// the COO row ids of the CSR (built once per context, shared with EU)
+bl_status bl_attr_launch(bl_ctx *h, const BLKParams &k, cudaStream_t st);
+bl_status bl_coo_rows(bl_ctx *h, cudaStream_t st);

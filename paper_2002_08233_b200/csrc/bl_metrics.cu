@@ -67,14 +67,15 @@ extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu
   BLM_ALLOC(h, S_EU_STATS, stats, sizeof(double) * 8);
   const float2 *xy = reinterpret_cast<const float2 *>(d_xy);
   DevBuf row;
-  const bool fresh = h->m_cap[S_EU_ROW] == 0;
-  BLM_ALLOC(h, S_EU_ROW, row, sizeof(int) * std::max<size_t>(1, h->nnz));
+  const bool fresh = h->d_coo_row == nullptr;
   int launches = 4;
   BL_CUDA(h, mark(h, 0, st));
   if (fresh) {  // once per context: the COO row ids of the CSR entries
-    blm_coo_rows<<<nb, BLM_NT, 0, st>>>(h->d_rowptr, h->n, row.as<int>());
+    bl_status s = bl_coo_rows(h, st);
+    if (s != BL_OK) return s;
     ++launches;
   }
+  row.p = h->d_coo_row;
   for (int pass = 0; pass < 2; ++pass) {
     blm_eu_pass<<<nb, BLM_NT, 0, st>>>(row.as<int>(), h->d_colidx, xy, (long long)h->nnz, pass,
                                         stats.as<double>(), part.as<double2>());

@@ -36,14 +36,7 @@ __device__ __forceinline__ double blm_block_sum(double v, double *sh_warp) {
 }
 
 // ---------------------------------------------------------------- EU (M2)
-// COO row ids of the CSR entries (row[k] = i for rowptr[i] <= k < rowptr[i+1]),
-// built once per context on the first EU call: makes the EU passes purely
-// entry-parallel and coalesced whatever the degree skew.
-__global__ void blm_coo_rows(const int *rowptr, int n, int *row) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) row[k] = i;
-}
-
+// (COO row ids: bla_coo_rows in bl_attr.cuh, built once per context)
 // pass 0: part[b] = (sum of edge lengths, edge count); pass 1: part[b] =
 // sum (l - mu)^2 with mu = stats[0] / stats[1] from pass 0.  Each undirected
 // edge once (entries with j > i).  Entry-parallel, grid-stride with a fixed
