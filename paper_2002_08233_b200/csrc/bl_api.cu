@@ -455,17 +455,19 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // coordinates (16-byte cp.async of target pairs)
   // kernel variant: r != -1 -> <512,8,-1> (two MUFU per pair);
   // very large batches (b n >= 5e8, e.g. 2^20 vertices x 1024) -> <256,16,6>
-  // (fewer, wider warps amortise best); latency-bound batches (b n <=
-  // BL_SMALL_PAIRS, default 2^24) -> <512,2,1>: 64-target tiles and >= 4-slot
-  // sub-ranges spread each batch's small sweep over all 16 warps instead of
-  // a few long units (measured: C2 -17 %, C3 b=256 -29 %, C4 -23 % per batch
-  // vs <512,8,2>); else <512,8,2>.  BL_NT / BL_T / BL_TP (read at bl_create)
+  // (fewer, wider warps amortise best); latency-bound batches (b <= 512 and
+  // b n <= BL_SMALL_PAIRS, default 2^24) -> <512,2,1>: 64-target tiles and
+  // >= 4-slot sub-ranges spread each batch's small sweep over all 16 warps
+  // instead of a few long units (measured: C2 -17 %, C3 b=256 -29 %, C4 -23 %
+  // per batch vs <512,8,2>; C3 b=1024 +34 %: its 16 tiles keep <512,8,2>);
+  // else <512,8,2>.  BL_NT / BL_T / BL_TP (read at bl_create)
   // pin a variant.
   model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
   const long long bn = (long long)b * n;
   const bool user_variant = getenv("BL_NT") || getenv("BL_T") || getenv("BL_TP");
   const bool wide = !user_variant && bn >= 500000000LL;
-  const bool small_b = !user_variant && bn <= (long long)env_int("BL_SMALL_PAIRS", 1 << 24);
+  const bool small_b = !user_variant && b <= 512 &&
+                       bn <= (long long)env_int("BL_SMALL_PAIRS", 1 << 24);
   const BLVariant *vt = k.rmode != 0 ? find_variant(512, 8, -1)
                         : wide && !attr_only ? find_variant(256, 16, 6)
                         : small_b && !attr_only ? find_variant(512, 2, 1)

@@ -374,7 +374,19 @@ __device__ __forceinline__ float bl_model_coef(const P &p, float d2, float rs, f
 // CTA-scope release/acquire fence for the task-queue handshakes in shared
 // memory (a flag written after data / read before data): fence.acq_rel.cta,
 // not the sequentially consistent MEMBAR.SC.CTA of __threadfence_block().
-__device__ __forceinline__ void bl_fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+#ifndef BL_FENCE_ACQREL_CTA
+#define BL_FENCE_ACQREL_CTA 0
+#endif
+#ifndef BL_POLL_RELAXED
+#define BL_POLL_RELAXED 0
+#endif
+__device__ __forceinline__ void bl_fence_cta() {
+#if BL_FENCE_ACQREL_CTA
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
+#else
+  __threadfence_block();  // measured faster here than fence.acq_rel.cta
+#endif
+}
 __device__ __forceinline__ unsigned bl_ld_relaxed(const unsigned *p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1000,29 +1012,51 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
   }
   const float2 ci = bl_src_get(src4, (v - c) / G);
   const float2 *row = p.part + (size_t)(q % p.part_nbuf) * p.b * G + (size_t)local * G;
-  float rx = 0.f, ry = 0.f;
-#pragma unroll 8
-  for (int cc = lane; cc < G; cc += 32) {
-    const float2 t = __ldcg(row + cc);
-    rx += t.x;
-    ry += t.y;
+  // latency: the staged row's neighbour gather (one entry per lane) and the
+  // row bounds of a long row are issued BEFORE the partial-row loads are
+  // consumed, so the two dependent L2 trips of an update overlap
+  int j_st = -1;
+  float2 cj_st = ci;
+  if (srow && lane < sdeg) {
+    j_st = srow[lane];
+    cj_st = (j_st >= plo && j_st < phi) ? __ldcg(pend_prev + (j_st - plo)) : __ldcg(p.xy + j_st);
   }
-  if (BL_CHK_ON)
-    for (int cc = lane; cc < G; cc += 32)
-      BL_CHK(__ldcg(p.part_st + (size_t)(row - p.part) + cc) == (unsigned)q + 1u, BLC_PART_STAMP,
-             q, cc);
   int k0 = 0, k1 = 0;
   if (!srow) {
     k0 = __ldg(p.rowptr + v);
     k1 = __ldg(p.rowptr + v + 1);
   }
+  float rx = 0.f, ry = 0.f;
+  {
+    float2 pr[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int cc = lane + 32 * u;
+      pr[u] = cc < G ? __ldcg(row + cc) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (lane + 32 * u < G) {
+        rx += pr[u].x;
+        ry += pr[u].y;
+      }
+    for (int cc = lane + 256; cc < G; cc += 32) {  // G > 256 (not on B200's 148 SMs)
+      const float2 t = __ldcg(row + cc);
+      rx += t.x;
+      ry += t.y;
+    }
+  }
+  if (BL_CHK_ON)
+    for (int cc = lane; cc < G; cc += 32)
+      BL_CHK(__ldcg(p.part_st + (size_t)(row - p.part) + cc) == (unsigned)q + 1u, BLC_PART_STAMP,
+             q, cc);
   const float rep = (p.flags & 1u) ? 0.f : p.ck2;
   float sx = 0.f, sy = 0.f;
   auto scan_row = [&](auto fast) {
-    if (srow) {  // staged row: one entry per lane
+    if (srow) {  // staged row: one entry per lane (gathered above)
       if (lane < sdeg) {
-        const int j = srow[lane];
-        const float2 cj = (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        const int j = j_st;
+        const float2 cj = cj_st;
         if (BL_CHK_ON) bl_chk_nb(p, q, j, plo, phi);
         const float dx = cj.x - ci.x, dy = cj.y - ci.y;
         const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
@@ -1224,12 +1258,18 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
                                                unsigned bar_target, int need = -1) {
   const int lane = threadIdx.x & 31;
   int go = 0;
-  // poll with a relaxed load (an acquire load costs an L1 invalidation per
-  // poll); the claimant alone then acquires with a GPU-scope fence
+  // BL_POLL_RELAXED=1: poll with a relaxed load, the claimant alone then
+  // acquires with a GPU-scope fence (measured slower than acquire polls,
+  // DESIGN.md §13)
+#if BL_POLL_RELAXED
   if (lane == 0 && ((int)(bl_ld_relaxed(p.bar) - bar_target) >= 0 || (BL_CHK_ON && p.chk_break))) {
     go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
     if (go) asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
+#else
+  if (lane == 0 && ((int)(bl_ld_acquire(p.bar) - bar_target) >= 0 || (BL_CHK_ON && p.chk_break)))
+    go = atomicCAS(&sh.ctrl_claim, f.ph - 1, f.ph) == f.ph - 1;
+#endif
 #ifdef BL_PHASE_TS
   if (go && p.prof) sh.ts_claim = clock64();
 #endif
