@@ -79,7 +79,7 @@ extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu
   for (int pass = 0; pass < 2; ++pass) {
     blm_eu_pass<<<nb, BLM_NT, 0, st>>>(row.as<int>(), h->d_colidx, xy, (long long)h->nnz, pass,
                                         stats.as<double>(), part.as<double2>());
-    blm_reduce_parts<<<1, 32, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
+    blm_reduce_parts<<<1, BLM_RT, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
   }
   BL_CUDA(h, cudaGetLastError());
   BL_CUDA(h, mark(h, 1, st));
@@ -143,7 +143,7 @@ extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sour
   void *args[] = {&k};
   BL_CUDA(h, mark(h, 0, st));
   BL_CUDA(h, cudaLaunchCooperativeKernel((void *)blm_stress_kernel, dim3(G), dim3(BLM_NT), args, 0, st));
-  blm_stress_reduce<<<1, 32, 0, st>>>(k.accA, k.accB, k.accN, k.work, G * BLM_NT,
+  blm_stress_reduce<<<1, BLM_RT, 0, st>>>(k.accA, k.accB, k.accN, k.work, G * BLM_NT,
                                       out4.as<double>(), outN.as<unsigned long long>());
   BL_CUDA(h, cudaGetLastError());
   BL_CUDA(h, mark(h, 1, st));
@@ -189,7 +189,7 @@ extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
   blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx,
                                                 reinterpret_cast<const float2 *>(d_xy), n,
                                                 queries ? d_q.as<int>() : nullptr, nq, jac.as<double>());
-  blm_np_reduce<<<1, 32, 0, st>>>(jac.as<double>(), nq, out.as<double>(), cnt.as<int>());
+  blm_np_reduce<<<1, BLM_RT, 0, st>>>(jac.as<double>(), nq, out.as<double>(), cnt.as<int>());
   BL_CUDA(h, cudaGetLastError());
   BL_CUDA(h, mark(h, 1, st));
   int c = 0;
