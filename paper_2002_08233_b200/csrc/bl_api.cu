@@ -530,6 +530,31 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     const int tile_slots = ((b + 32 * vt->T - 1) / (32 * vt->T)) * 32 * vt->T;
     k.red_cap = std::min(k.red_cap, 2 * k.nsub_max * tile_slots);
   }
+  // latency driver (bl_run_lat): updater warps = owned vertices per batch
+  // per CTA (<= half the warps), every tile's clean sub-ranges plus one in
+  // each half of red.  The default where the pair work per batch is small
+  // (b n <= BL_SMALL_PAIRS, 2^24): measured same box vs the asynchronous
+  // driver, us per dependent batch: C2 6.17 -> 4.28, C3 b=256 5.83 -> 4.21,
+  // C3 b=1024 10.95 -> 7.36, C4 8.54 -> 6.72.  BL_LAT=1 / 0
+  // forces it on / off; BL_ASYNC=0/1 (pipelined / asynchronous) also turns
+  // it off.
+  {
+    const int lat_env = env_int("BL_LAT", -1);
+    const bool lat_auto = lat_env < 0 && async_env < 0 &&
+                          bn <= (long long)env_int("BL_SMALL_PAIRS", 1 << 24);
+    const int ntt = (b + 32 * vt->T - 1) / (32 * vt->T);
+    const int U = (b + G - 1) / G;
+    const int red_lat = red_cap_for(k.chunk4);
+    const bool lat_ok = k.pipelined && U <= vt->NT / 64 && ntt <= BL_NTT_MAX &&
+                        red_lat / 2 / (ntt * 32 * vt->T) >= 2 && n >= 2 * G;
+    if (lat_ok && (lat_env == 1 || lat_auto)) {
+      k.pipelined = 3;
+      k.part_nbuf = 2;
+      k.red_cap = red_lat;
+      k.guided = env_int("BL_GUIDED", 1);
+      k.nsub_max = std::max(2, env_int("BL_NSUB", 6));
+    }
+  }
 #ifdef BL_CHECKED
   // checked build: zeroed violation record and stamps for this launch
   if (!h->d_chk) {
@@ -553,6 +578,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   h->driver_last = forces_mode ? "two-barrier"
+                   : k.pipelined == 3 ? "latency"
                    : k.pipelined == 2 ? "async"
                    : k.pipelined      ? "pipelined"
                                       : "two-barrier";

@@ -214,7 +214,9 @@ enum {
   BLC_TOKENS = 6,       // more completion tokens than the phase needs
   BLC_BOUNDS = 7,       // index out of range (part / pend / red / src)
   BLC_PHASEU_STAMP = 8, // two-barrier phase U read a partial not from its batch
-  BLC_SLOT_GEN = 9      // async: a phase entered a slot not released for it
+  BLC_SLOT_GEN = 9,     // async: a phase entered a slot not released for it
+  BLC_LAT_TGT = 10,     // latency driver: a staged target not the committed coordinate
+  BLC_LAT_CLEAN = 11    // latency driver: a clean partial not the sum over the clean sources
 };
 
 // ---- batch randomisation (§4.3.3; readings R1-R2 of DESIGN.md §3):
@@ -376,6 +378,9 @@ __device__ __forceinline__ float bl_model_coef(const P &p, float d2, float rs, f
 // not the sequentially consistent MEMBAR.SC.CTA of __threadfence_block().
 #ifndef BL_FENCE_ACQREL_CTA
 #define BL_FENCE_ACQREL_CTA 0
+#endif
+#ifndef BL_EARLY_TGT
+#define BL_EARLY_TGT 1
 #endif
 #ifndef BL_POLL_RELAXED
 #define BL_POLL_RELAXED 0
@@ -881,6 +886,7 @@ __device__ __forceinline__ void bl_refresh_resident(const BLKParams &p, const BL
 // read from pend when j is in batch ph-1 and from xy otherwise.  This is
 // exactly the frozen-batch semantics of Alg. 2.
 #define BL_ETASK_MAX 64  // owned vertices per CTA per batch (b <= 64·G)
+#define BL_RSTAGE 32     // owned vertices per CTA per batch whose CSR rows are staged
 #define BL_NTT_MAX 32    // target tiles per batch (BL_TGT_CAP / (32 T), T >= 2)
 
 struct BLShared {
@@ -907,9 +913,12 @@ struct BLShared {
   // by the control task of the phase that sweeps the batch, used by the
   // update tasks one phase later (two fewer dependent L2 round trips on the
   // per-batch critical path); rowq = the batch they belong to
-  int rows[2][BL_ETASK_MAX][32];
-  int rdeg[2][BL_ETASK_MAX];
-  int rowq[2];
+  // three buffers (batch q -> q % 3): the async driver stages batch ph+1 in
+  // the control task of phase ph, after publishing `ready`, a phase before
+  // its update tasks need it; only the first BL_RSTAGE owned vertices
+  int rows[3][BL_RSTAGE][32];
+  int rdeg[3][BL_RSTAGE];
+  int rowq[3];
   // asynchronous-phase driver (bl_run_async): per phase parity s = ph & 1
   int a_unit[2];               // next sweep unit
   int a_tdone[2][BL_NTT_MAX];  // finished units per target tile
@@ -918,6 +927,13 @@ struct BLShared {
   int a_exit[2];               // warps that left the phase
   int a_gen[2];                // the phase allowed to use slot s next
   int a_updph;                 // last phase whose update tasks all finished
+  // latency driver (bl_run_lat): monotone phase stamps + per-parity counters
+  int l_applied;               // last batch whose owned updates are in src4
+  int l_cleanp[2];             // phase whose clean partials are combined, per parity
+  int l_dec;                   // last phase whose stop decision is taken
+  int l_join[2];               // updater warps that finished phase q's update
+  int l_unit[2], l_exit[2], l_gen[2], l_tiles[2];
+  int l_tdone[2][BL_NTT_MAX];
 #ifdef BL_PHASE_TS
   // critical-path timestamps (profiling builds, -DBL_PHASE_TS; they cost ~3 %
   // at C5 even when disabled at run time, so they are compiled out by
@@ -1158,8 +1174,8 @@ __device__ __forceinline__ void bl_stage_rows_warp(const BLKParams &p, int q, BL
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b, hi = min(lo + p.b, p.n);
   const int v0 = lo + ((c - lo % G) + G) % G;
-  const int owned = v0 < hi ? (hi - 1 - v0) / G + 1 : 0;
-  const int buf = q & 1;
+  const int owned = min(BL_RSTAGE, v0 < hi ? (hi - 1 - v0) / G + 1 : 0);
+  const int buf = q % 3;
   // two L2 round trips in all (latency is the cost here: this runs on the
   // per-batch critical path): the row bounds of up to 32 owned vertices in
   // one load per lane, then the rows of 8 vertices at a time, every load
@@ -1191,7 +1207,10 @@ __device__ __forceinline__ void bl_stage_rows_warp(const BLKParams &p, int q, BL
     }
   }
   __syncwarp();
-  if (lane == 0) sh.rowq[buf] = q;
+  if (lane == 0) {
+    bl_fence_cta();  // rows before rowq (the async driver stages after `ready`)
+    *(volatile int *)&sh.rowq[buf] = q;
+  }
 }
 
 // Writes that other CTAs read after barrier ph (part, pend, xy commits) are
@@ -1282,6 +1301,16 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
   __syncwarp();  // order the lanes' reads after lane 0's acquire
   bool stop = false;
   const int nb = p.nb;
+  // async driver: the next batch's targets were last written by batch
+  // ph+1-nb, committed by the control task of phase ph+3-nb <= ph-1 when
+  // nb >= 4, so their copy can be in flight while this task commits (one L2
+  // round trip for both); the staging buffer's last readers (phase ph-1's
+  // units) finished before barrier ph-1
+  const bool early_tgt = BL_EARLY_TGT && need >= 0 && nb >= 4 && f.ph + 1 < f.P;
+  if (early_tgt) {
+    const int lo_n = ((f.ph + 1) % nb) * p.b;
+    bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), f.tgt_next);
+  }
   if (f.q2 >= 0 && bl_closes_iteration(f.q2, nb, f.P)) {
     const int it = f.q2 / nb;
     const double E = bl_energy_sum_warp(p, it);
@@ -1303,10 +1332,13 @@ __device__ __forceinline__ bool bl_try_control(const BLKParams &p, const BLPhase
       bl_token(p, sh, f, need);
     }
   }
-  if (!stop && f.ph + 1 < f.P) {
+  if (!stop && f.ph + 1 < f.P && !early_tgt) {
     const int lo_n = ((f.ph + 1) % nb) * p.b;
     bl_prefetch_targets_warp(p, lo_n, min(p.b, p.n - lo_n), f.tgt_next);
   }
+  // (measured: staging the rows after `ready` -- even a phase ahead -- costs
+  // ~1 us per batch at C2 / C3: the control warp is the awake warp that
+  // picks up the next task)
   if (!stop && f.ph < f.P) bl_stage_rows_warp(p, f.ph, sh);
   // async driver: the targets must have landed before `ready` lets warps
   // into phase ph+1 (the pipelined driver waits at its phase-end barrier)
@@ -1349,9 +1381,9 @@ __device__ __forceinline__ bool bl_try_update(const BLKParams &p, const BLPhase 
   t = __shfl_sync(0xffffffffu, t, 0);
   if (t >= f.owned) return false;
   bl_fence_cta();  // acquire the control warp's publication
-  const int buf = f.q1 & 1;
+  const int buf = f.q1 % 3;
   const volatile BLShared &vsh = sh;
-  const bool staged = vsh.rowq[buf] == f.q1 && vsh.rdeg[buf][t] >= 0;
+  const bool staged = t < BL_RSTAGE && vsh.rowq[buf] == f.q1 && vsh.rdeg[buf][t] >= 0;
   bl_jitter(p, 21);
   bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t],
                 staged ? sh.rows[buf][t] : nullptr, staged ? vsh.rdeg[buf][t] : 0);
@@ -1542,8 +1574,12 @@ __device__ __forceinline__ bool bl_try_update_a(const BLKParams &p, const BLPhas
   t = __shfl_sync(0xffffffffu, t, 0);
   if (t >= f.owned) return false;
   bl_fence_cta();  // acquire the control warp's publication
-  const int buf = f.q1 & 1;
-  const bool staged = vs.rowq[buf] == f.q1 && vs.rdeg[buf][t] >= 0;
+  const int buf = f.q1 % 3;
+  bool staged = t < BL_RSTAGE && vs.rowq[buf] == f.q1;
+  if (staged) {
+    bl_fence_cta();  // rowq before the rows (the async driver stages them after `ready`)
+    staged = vs.rdeg[buf][t] >= 0;
+  }
   bl_jitter(p, 22);
   bl_update_one(p, f.q1, f.v0 + t * gridDim.x, f.step_u, src4, &sh.e_task[t],
                 staged ? sh.rows[buf][t] : nullptr, staged ? vs.rdeg[buf][t] : 0);
@@ -1799,6 +1835,350 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
   if (c == 0 && threadIdx.x == 0) *p.iters_done = sh.done_iters;
 }
 
+// ---------------------------------------------------------------------------
+// Latency driver (bl_run_lat, BLKParams::pipelined == 3): the per-batch chain
+// of small batches (C2-C4: 0.3-2 us of pair work per batch against a grid
+// barrier + dependent L2 round trips) with no task queues and no hand-offs
+// on it.  Warps 0..U-1 (U = max owned vertices per batch per CTA) are
+// updaters, the others sweepers.  Phase q (targets = batch q):
+//   sweepers  sweep the CTA's resident sources EXCEPT its owned members of
+//             batch q-1, M(q-1), against batch q's targets (read from xy,
+//             where batch q is committed: its last update, batch q-nb, was
+//             committed in phase q-nb+2 <= q-2), as soon as M(q-2) is
+//             applied -- one phase ahead of the chain; tile partials are
+//             combined in sub-range order into the clean partial C_q (red,
+//             parity q & 1), the targets kept in tgt[q & 1] for D(q);
+//   updaters  each loads its next member's CSR row, spins on barrier q-1
+//             itself, updates that member of M(q-1) (Alg. 2 for one vertex:
+//             partial row, CSR attraction, fp64 step) and joins; the LAST
+//             updater to join continues the chain: publishes M(q-1), books
+//             the energy, commits M(q-2) to xy, adds the sweep of the dirty
+//             float4s (M(q-1)'s slots at their new coordinates) to C_q for
+//             every target in fixed order -> part, arrives at barrier q.
+// Same values and summation order as the asynchronous driver's (the clean
+// sub-ranges in order, then the dirty one).  Needs nb >= 4.
+template <int T, int TP>
+__device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, float2 *tgt,
+                                           float2 *red, BLShared &sh) {
+  const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = p.nb;
+  const long long ptot = (long long)p.iters * nb;
+  const bool mb_stop = p.max_batches > 0 && p.max_batches <= ptot;
+  const int P = mb_stop ? p.max_batches : (int)ptot;
+  const int half = p.red_cap / 2;
+  // updater warps: >= the owned vertices per batch per CTA, >= 4 (D(q)'s
+  // target chunks are shared), <= half the warps (host checks the first)
+  const int U = min(BL_NW / 2, max(4, (p.b + G - 1) / G));
+  const volatile BLShared &vs = sh;
+  if (threadIdx.x == 0) {
+    sh.done_iters = mb_stop ? (P - 1) / nb : p.iters;
+    sh.e_prev = 0.0;
+    sh.e_acc = 0.0;
+    sh.l_applied = -1;
+    sh.l_cleanp[0] = sh.l_cleanp[1] = -1;
+    sh.l_dec = -1;
+    for (int k = 0; k < 2; ++k) {
+      sh.l_join[k] = sh.l_unit[k] = sh.l_exit[k] = sh.l_tiles[k] = 0;
+      sh.l_gen[k] = k;
+      for (int t = 0; t < BL_NTT_MAX; ++t) sh.l_tdone[k][t] = 0;
+    }
+  }
+  __syncthreads();
+
+  // owned members of batch q in this CTA: v0(q), v0 + G, ... (count m(q))
+  auto members = [&](int q, int &v0, int &m) {
+    const int lo = (q % nb) * p.b, hi = min(lo + p.b, p.n);
+    v0 = lo + ((c - lo % G) + G) % G;
+    m = v0 < hi ? (hi - 1 - v0) / G + 1 : 0;
+  };
+
+  if (warp >= U) {
+    // ---------------- sweepers ----------------
+    unsigned ns = 32;
+    for (int r = 0; r < P; ++r) {
+      const int s = r & 1;
+      for (;;) {  // gate: M(r-2) applied, parity slot free
+        if (vs.stop_flag) return;
+        if (vs.l_applied >= r - 2 && vs.l_gen[s] == r) break;
+        __nanosleep(ns);
+        ns = min(2 * ns, 256u);
+      }
+      ns = 32;
+      bl_fence_cta();
+      int v0 = 0, m = 0;
+      if (r >= 1) members(r - 1, v0, m);
+      const int lo = (r % nb) * p.b, bt = min(p.b, p.n - lo);
+      const BLGeom geo = bl_geom(c, G, p.n, m > 0 ? (v0 - c) / G : 0, m);
+      const BLUnits Un = bl_units(bt, T, geo.clean4, true, half, p.nsub_max, p.min_unit4);
+      const int n_clean = Un.ntt * Un.nc, stride = Un.ntt * 32 * T;
+      float2 *red_s = red + s * half;
+      float2 *tgt_s = tgt + s * BL_TGT_CAP;
+      const int dw = geo.d_hi - geo.d_lo;
+      for (;;) {
+        int g = n_clean;
+        if (lane == 0) g = atomicAdd(&sh.l_unit[s], 1);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= n_clean) break;
+        bl_jitter(p, 31);
+        const int tile = g % Un.ntt, sub = g / Un.ntt;
+        float tx[T], ty[T];
+        bl_f2 AX[T], AY[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          const int idx = tile * 32 * T + k * 32 + lane;
+          const float2 t = idx < bt ? __ldcg(p.xy + lo + idx) : make_float2(0.f, 0.f);
+          if (sub == 0 && idx < bt) tgt_s[idx] = t;  // for D(r)
+          tx[k] = t.x;
+          ty[k] = t.y;
+          AX[k] = AY[k] = f2pack(0.f, 0.f);
+        }
+        const int a = bl_guided_start(sub, Un.nc, geo.clean4, p.guided);
+        const int e = bl_guided_start(sub + 1, Un.nc, geo.clean4, p.guided);
+        if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY, p.r_half);
+        if (e > geo.d_lo)
+          bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY, p.r_half);
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          const int idx = tile * 32 * T + k * 32 + lane;
+          float ax0, ax1, ay0, ay1;
+          f2unpack(AX[k], ax0, ax1);
+          f2unpack(AY[k], ay0, ay1);
+          if (idx < bt) red_s[sub * stride + idx] = make_float2(ax0 + ax1, ay0 + ay1);
+        }
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          bl_fence_cta();
+          last = atomicAdd(&sh.l_tdone[s][tile], 1) == Un.nc - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {  // combine the tile's clean sub-ranges in order into slot 0
+          bl_fence_cta();
+          if (Un.nc > 1) {
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+              const int idx = tile * 32 * T + k * 32 + lane;
+              if (idx < bt) {
+                float2 acc = red_s[idx];
+                for (int sb = 1; sb < Un.nc; ++sb) {
+                  const float2 v = red_s[sb * stride + idx];
+                  acc.x += v.x;
+                  acc.y += v.y;
+                }
+                red_s[idx] = acc;
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            bl_fence_cta();
+            if (atomicAdd(&sh.l_tiles[s], 1) == Un.ntt - 1) {
+              bl_fence_cta();
+              *(volatile int *)&sh.l_cleanp[s] = r;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      // leave phase r; the last sweeper out resets parity s for phase r+2
+      if (lane == 0 && atomicAdd(&sh.l_exit[s], 1) == BL_NW - U - 1) {
+        bl_fence_cta();
+        sh.l_unit[s] = sh.l_exit[s] = sh.l_tiles[s] = 0;
+        for (int t = 0; t < BL_NTT_MAX; ++t) sh.l_tdone[s][t] = 0;
+        bl_fence_cta();
+        *(volatile int *)&sh.l_gen[s] = r + 2;
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---------------- updaters ----------------
+  // U warps synchronised by the hardware named barrier 1 (bar.sync 1, 32 U):
+  // warp 0 alone polls the grid barrier; every updater warp updates at most
+  // one member and takes a share of D(q)'s target chunks; warp 0 arrives.
+  double step_u = p.step0;
+  int *myrow = sh.rows[0][warp];  // this warp's staged CSR row (<= 32 entries)
+  const unsigned nthr = 32u * (unsigned)U;
+  auto ubar = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory"); };
+  for (int q = 0; q <= P; ++q) {
+    const int s = q & 1;
+    int v0 = 0, m = 0;
+    if (q >= 1) {
+      members(q - 1, v0, m);
+      if (q - 1 > 0 && (q - 1) % nb == 0) step_u = step_u * p.cooling;
+    }
+#ifdef BL_PHASE_TS
+    long long t_det = 0;
+#endif
+    if (q >= 1) {
+      // this warp's member: its CSR row (constant) before the barrier
+      int deg = -1;
+      if (warp < m) {
+        const int v = v0 + warp * G;
+        const int k0 = __ldg(p.rowptr + v);
+        deg = __ldg(p.rowptr + v + 1) - k0;
+        if (deg <= 32 && lane < deg) myrow[lane] = __ldg(p.colidx + k0 + lane);
+        __syncwarp();
+      }
+      if (warp == 0) {
+        // barrier q-1 (every CTA's partials of batch q-1)
+        const unsigned target = (unsigned)q * (unsigned)G;
+        if (lane == 0)
+          while ((int)(bl_ld_acquire(p.bar) - target) < 0) {
+          }
+        __syncwarp();
+        // iteration energy of batch q-2's iteration (booked before barrier
+        // q-1) and the tol decision, identical in every CTA
+        const int q2 = q - 2;
+        if (q2 >= 0 && bl_closes_iteration(q2, nb, P)) {
+          const int it = q2 / nb;
+          const double E = bl_energy_sum_warp(p, it);
+          if (c == 0 && lane == 0) p.energy[it] = E;
+          if (lane == 0) {
+            if (q2 % nb == nb - 1 && q2 < P - 1 && p.tol > 0.0 && it > 0 &&
+                fabs(E - sh.e_prev) < p.tol) {
+              sh.done_iters = it + 1;
+              sh.stop_flag = 1;
+            }
+            sh.e_prev = E;
+          }
+        }
+      }
+      ubar();  // barrier q-1 seen (bar.sync orders warp 0's acquire before the reads below)
+#ifdef BL_PHASE_TS
+      t_det = clock64();
+#endif
+      bl_jitter(p, 32);
+      if (vs.stop_flag == 0 && warp < m)
+        bl_update_one(p, q - 1, v0 + warp * G, step_u, src4, &sh.e_task[warp],
+                      deg <= 32 ? myrow : nullptr, deg <= 32 ? deg : 0);
+    }
+    ubar();  // every member of M(q-1) updated (src4, pend, e_task)
+#ifdef BL_PHASE_TS
+    const long long t_join = clock64();
+#endif
+    const bool stop = vs.stop_flag != 0;
+    if (stop || q == P) {
+      if (warp == 0) {
+        if (!stop && q == P) {
+          // the last batch's energy: book it, arrive at barrier P, wait for
+          // every CTA's, sum (CTA 0 writes the trace)
+          if (lane == 0) {
+            double e = sh.e_acc;
+            for (int i = 0; i < m; ++i) e += sh.e_task[i];
+            p.e_cta[(((P - 1) / nb) & 1) * G + c] = e;
+            asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+            const unsigned target = (unsigned)(P + 1) * (unsigned)G;
+            while ((int)(bl_ld_acquire(p.bar) - target) < 0) {
+            }
+          }
+          __syncwarp();
+          const double E = bl_energy_sum_warp(p, (P - 1) / nb);
+          if (c == 0 && lane == 0) p.energy[(P - 1) / nb] = E;
+        }
+        // final positions: every owned source (all updates are done: after
+        // barrier P, or a stop decided identically everywhere after barrier q-1)
+        const int mc = c < p.n ? (p.n - 1 - c) / G + 1 : 0;
+        for (int k = lane; k < mc; k += 32) p.xy[c + (size_t)k * G] = bl_src_get(src4, k);
+        if (lane == 0) {
+          *(volatile int *)&sh.stop_flag = 1;  // release the sweepers
+          if (c == 0) *p.iters_done = sh.done_iters;
+        }
+      }
+      break;
+    }
+    if (warp == 0) {
+      // (a) publish M(q-1): sweepers of phase q+1 may start; (b) energy
+      if (lane == 0 && q >= 1) {
+        *(volatile int *)&sh.l_applied = q - 1;
+        double e = sh.e_acc;
+        for (int i = 0; i < m; ++i) e += sh.e_task[i];  // task order
+        sh.e_acc = e;
+        if (bl_closes_iteration(q - 1, nb, P)) {
+          p.e_cta[(((q - 1) / nb) & 1) * G + c] = e;
+          sh.e_acc = 0.0;
+        }
+      }
+    }
+    // (c) commit M(q-2) to xy (read as committed after barrier q)
+    if (q >= 2 && warp == U - 1) bl_commit_warp(p, q - 2, src4);
+    // (d) D(q): clean partial + the dirty float4s, per target, into part;
+    // target chunks of 32 T split over the updater warps
+    bl_jitter(p, 33);
+    while (vs.l_cleanp[s] != q) {
+    }
+    bl_fence_cta();
+#ifdef BL_PHASE_TS
+    const long long t_clean = clock64();
+#endif
+    {
+      const int lo = (q % nb) * p.b, bt = min(p.b, p.n - lo);
+      const BLGeom geo = bl_geom(c, G, p.n, m > 0 ? (v0 - c) / G : 0, m);
+      const float2 *red_s = red + s * half;
+      const float2 *tgt_s = tgt + s * BL_TGT_CAP;
+      float2 *part = p.part + (size_t)(q % p.part_nbuf) * p.b * G;
+      for (int base = warp * 32 * T; base < bt; base += U * 32 * T) {
+        float tx[T], ty[T];
+        bl_f2 AX[T], AY[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          const int idx = base + k * 32 + lane;
+          const float2 t = idx < bt ? tgt_s[idx] : make_float2(0.f, 0.f);
+          tx[k] = t.x;
+          ty[k] = t.y;
+          AX[k] = AY[k] = f2pack(0.f, 0.f);
+        }
+        if (geo.d_lo < geo.d_hi)
+          bl_sweep_range<T, TP>(src4, geo.d_lo, geo.d_hi, geo.full4, tx, ty, AX, AY, p.r_half);
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          const int idx = base + k * 32 + lane;
+          if (idx < bt) {
+            float ax0, ax1, ay0, ay1;
+            f2unpack(AX[k], ax0, ax1);
+            f2unpack(AY[k], ay0, ay1);
+            float2 acc = red_s[idx];
+            if (geo.d_lo < geo.d_hi) {
+              acc.x += ax0 + ax1;
+              acc.y += ay0 + ay1;
+            }
+            part[(size_t)idx * G + c] = acc;
+            if (BL_CHK_ON) p.part_st[(size_t)(part - p.part) + (size_t)idx * G + c] = (unsigned)q + 1u;
+          }
+        }
+      }
+    }
+    bl_jitter(p, 34);
+    ubar();  // D(q), the commit and the energy booking are done
+    // (e) arrive at barrier q
+    if (warp == 0 && lane == 0) {
+#ifdef BL_PHASE_TS
+      const long long t_d = clock64();
+#endif
+      asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+#ifdef BL_PHASE_TS
+      // CTA-0 timeline (async_profile.py, latency driver): previous arrival ->
+      // barrier seen -> updates done -> clean partial ready -> D done -> arrival
+      const long long t_arr = clock64();
+      if (p.prof && c == 0) {
+        unsigned long long *hp = p.prof + 8 + G;
+        if (q >= 1) {
+          hp[0] += (unsigned long long)(t_det - sh.ts_arr_prev);
+          hp[1] += (unsigned long long)(t_join - t_det);
+          hp[2] += (unsigned long long)(t_clean - t_join);
+          hp[3] += (unsigned long long)(t_d - t_clean);
+          hp[4] += (unsigned long long)(t_arr - t_d);
+          hp[5] += 1ull;
+          hp[6] += 1ull;
+        }
+        sh.ts_arr_prev = t_arr;
+      }
+#endif
+    }
+  }
+}
+
 template <int NT, int T, int TP>
 __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
   extern __shared__ float4 bl_smem[];
@@ -1814,7 +2194,7 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
     sh.ready = 0;
     sh.ctrl_claim = 0;
     sh.seen = 0;
-    sh.rowq[0] = sh.rowq[1] = -1;
+    sh.rowq[0] = sh.rowq[1] = sh.rowq[2] = -1;
   }
   int *unit_ctr = &sh.unit_ctr;
   double *e_warp = sh.e_warp;
@@ -1860,6 +2240,10 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
 
   if (p.pipelined == 2) {
     bl_run_async<T, TP>(p, src4, tgt, red, sh);
+    return;
+  }
+  if (p.pipelined == 3) {
+    bl_run_lat<T, TP>(p, src4, tgt, red, sh);
     return;
   }
   if (p.pipelined) {

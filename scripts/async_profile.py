@@ -47,7 +47,14 @@ with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
     G = torch.cuda.get_device_properties(0).multi_processor_count
     hp = pr[8 + G:8 + G + 8]
     mhz = float(a.mhz)
-    if hp.size >= 7 and hp[5] > 0:
+    if hp.size >= 7 and hp[5] > 0 and bl.bl_driver_name(lay.h) == "latency":
+        nph = hp[5]
+        out["cta0_timeline_us_per_batch"] = {
+            "barrier_and_detection": hp[0] / nph / mhz, "updates_to_join": hp[1] / nph / mhz,
+            "wait_clean_partial": hp[2] / nph / mhz, "dirty_sweep_D": hp[3] / nph / mhz,
+            "arrival_fence_red": hp[4] / nph / mhz, "phases": int(nph),
+            "total_batch_us": out["ms"] * 1e3 / (a.iters * -(-g.n // cfg.batch))}
+    elif hp.size >= 7 and hp[5] > 0:
         nph, nown = hp[5], max(hp[6], 1.0)
         out["cta0_timeline_us_per_batch"] = {
             "barrier_and_detection": hp[0] / nph / mhz, "control": hp[1] / nph / mhz,

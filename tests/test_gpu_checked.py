@@ -32,8 +32,10 @@ CASES = [
     ("C3b256", 2, {"BL_ASYNC": "0"}, {}),                  # pipelined driver
     ("C3b256", 2, {"BL_ASYNC": "1"}, {}),                  # asynchronous phases
     ("C3b256", 1, {"BL_PIPELINE": "0"}, {}),               # two-barrier driver
-    ("C4", 2, {}, {}),                                      # async (default), hub rows
-    ("C2", 3, {}, {}),                                      # pipelined (default)
+    ("C4", 2, {"BL_ASYNC": "1"}, {}),                      # async, hub rows
+    ("C4", 2, {}, {}),                                      # latency driver (default), hub rows
+    ("C2", 3, {"BL_ASYNC": "0"}, {}),                      # pipelined
+    ("C3b1024", 1, {"BL_LAT": "1"}, {"max_batches": 17}),  # latency driver, stop mid-iteration
     ("C3b1024", 1, {"BL_ASYNC": "1"}, {"max_batches": 17}),  # stop mid-iteration
     ("C3b256", 1, {}, {"shuffle_seed": 7}),                # randomised batches
     ("C2", 2, {"BL_ASYNC": "1", "BL_T": "2", "BL_TP": "1"}, {}),  # small-tile variant

@@ -471,7 +471,7 @@ def test_fuzz_shapes_one_iteration(case):
 # ---- the asynchronous-phase driver (bl_run_async, the default for nb >= 4)
 # vs the pipelined driver it replaces (BL_ASYNC=0) and vs the oracle
 _DRIVERS = [("async", {"BL_ASYNC": "1"}), ("pipelined", {"BL_ASYNC": "0"}),
-            ("two-barrier", {"BL_PIPELINE": "0"})]
+            ("two-barrier", {"BL_PIPELINE": "0"}), ("latency", {"BL_LAT": "1"})]
 
 
 def _with_env(monkeypatch, env):
@@ -494,14 +494,18 @@ def test_drivers_one_iteration_vs_oracle(name, driver, monkeypatch):
 
 
 @pytest.mark.parametrize("mb", [1, 2, 3, 4, 5, 43, 44, 45, 87])
-def test_async_driver_max_batches(mb, monkeypatch):
+@pytest.mark.parametrize("drv", [("async", {"BL_ASYNC": "1"}), ("latency", {"BL_LAT": "1"})],
+                         ids=["async", "latency"])
+def test_async_driver_max_batches(mb, drv, monkeypatch):
     """Every stop position of the phase pipeline: the first phases, a stop
     right at / after an iteration boundary (C3 b=256: 43 batches/iteration).
     Up to one iteration: vs the oracle run.  Beyond: shadowed (the chaos of
     DESIGN.md §6 makes free-running comparisons meaningless after the first
     iteration) -- batch mb-1 recomputed by the oracle from the GPU's own state
-    after mb-1 batches, with the step of its iteration."""
-    monkeypatch.setenv("BL_ASYNC", "1")
+    after mb-1 batches, with the step of its iteration.
+    Both one-barrier-per-batch drivers of small batches: asynchronous phases
+    and the latency driver."""
+    _with_env(monkeypatch, drv[1])
     g, xy0, cfg = build_config("C3b256")
     b = cfg.batch
     nb = -(-g.n // b)
@@ -525,25 +529,31 @@ def test_async_driver_max_batches(mb, monkeypatch):
     assert np.array_equal(np.delete(got, np.s_[lo:hi], 0), np.delete(prev, np.s_[lo:hi], 0))
 
 
-def test_async_driver_tol_stop_matches_pipelined(monkeypatch):
-    """The tol criterion stops both drivers at the same iteration."""
-    monkeypatch.setenv("BL_ASYNC", "1")
+@pytest.mark.parametrize("env", [{"BL_ASYNC": "1"}, {"BL_LAT": "1"}], ids=["async", "latency"])
+def test_async_driver_tol_stop_matches_pipelined(env, monkeypatch):
+    """The tol criterion stops the driver at the iteration its own
+    energy trace says (asynchronous and latency drivers), the pipelined one
+    with a trace of the same length."""
+    _with_env(monkeypatch, env)
     g, xy0, cfg = build_config("C4")
     _, full, _ = gpu_layout(g, xy0, iters=30, batch=256)
     tol = float(np.median(np.abs(np.diff(full)))) * 1.5
     stop = next(t for t in range(1, 30) if abs(full[t] - full[t - 1]) < tol) + 1
     _, tr, done = gpu_layout(g, xy0, iters=30, batch=256, tol=tol)
     assert done == stop and np.array_equal(tr, full[:stop])
+    monkeypatch.delenv("BL_LAT", raising=False)
     monkeypatch.setenv("BL_ASYNC", "0")
     _, tr2, done2 = gpu_layout(g, xy0, iters=30, batch=256, tol=tol)
     assert done2 <= 30 and tr2.shape == (done2,)
 
 
-@pytest.mark.parametrize("name", ["C4", "C5"])
-def test_async_driver_bitwise_repeatable(name, monkeypatch):
+@pytest.mark.parametrize("name,env", [("C4", {"BL_ASYNC": "1"}), ("C5", {"BL_ASYNC": "1"}),
+                                      ("C4", {"BL_LAT": "1"}), ("C3b1024", {"BL_LAT": "1"})])
+def test_async_driver_bitwise_repeatable(name, env, monkeypatch):
     """Fixed summation orders: repeated runs are bitwise identical whatever
-    warp ran which task (C5: 2 iterations = 512 dependent batches)."""
-    monkeypatch.setenv("BL_ASYNC", "1")
+    warp ran which task (C5: 2 iterations = 512 dependent batches); the
+    asynchronous and the latency drivers."""
+    _with_env(monkeypatch, env)
     g, xy0, cfg = build_config(name)
     p = _params(cfg, iters=2 if name == "C5" else 5)
     a, ea, _ = gpu_layout(g, xy0, **p)
@@ -604,12 +614,13 @@ def test_attraction_only_rejected_by_layout():
 
 
 @pytest.mark.parametrize("case", _FUZZ)
-def test_fuzz_shapes_async_forced(case, monkeypatch):
+@pytest.mark.parametrize("env", [{"BL_ASYNC": "1"}, {"BL_LAT": "1"}], ids=["async", "latency"])
+def test_fuzz_shapes_async_forced(case, env, monkeypatch):
     """The fuzzed shapes with the asynchronous-phase driver forced
     (BL_ASYNC=1; it takes over wherever the pipelined driver is eligible):
     one iteration vs the oracle, and a second run bitwise identical."""
     from blgen import ba_graph
-    monkeypatch.setenv("BL_ASYNC", "1")
+    _with_env(monkeypatch, env)
     kind, size, b, K, C, flags = case
     if kind == "rmat":
         g = rmat_graph(size, 8, 0.57, 0.19, 0.19, seed=size)
@@ -628,13 +639,12 @@ def test_fuzz_shapes_async_forced(case, monkeypatch):
     assert np.array_equal(got, again) and np.array_equal(tr, tr2)
 
 
-@pytest.mark.parametrize("name,expect", [("C2", "async"), ("C3b256", "async"),
-                                         ("C3b1024", "async"), ("C4", "async"),
+@pytest.mark.parametrize("name,expect", [("C2", "latency"), ("C3b256", "latency"),
+                                         ("C3b1024", "latency"), ("C4", "latency"),
                                          ("C1", "cluster"), ("C3b64", "cluster")])
 def test_default_driver_per_config(name, expect):
-    """The measured crossovers: single cluster for b n <= 1e6, asynchronous
-    phases above (with the <512,2,1> small-batch variant below b n = 2^24,
-    where it beats the pipelined driver)."""
+    """The measured crossovers: single cluster for b n <= 1e6, the latency
+    driver up to b n = 2^24, asynchronous phases above."""
     import torch
 
     import paper_2002_08233_b200 as bl
