@@ -712,7 +712,7 @@ def _golden_energy(name):
     import os
     path = os.path.join(os.path.dirname(__file__), "golden", f"energy_{name}.json")
     if not os.path.exists(path):
-        pytest.skip(f"{path} not generated (scripts/oracle_energy_golden.py {name})")
+        pytest.skip(f"{path} not generated (tests/tools/oracle_energy_golden.py {name})")
     with open(path) as fh:
         return json.load(fh)
 
@@ -722,7 +722,7 @@ def test_full_run_energy_vs_oracle_golden(name):
     """Full-run energy, the north star's "final energy within 1% relative"
     (Energy: P:539), with the chaos protocol of SURVEY.md §8(c): the
     oracle's traces (unperturbed fp64; 1-ulp-perturbed fp64 ensemble; fp32)
-    were written by scripts/oracle_energy_golden.py, which calls only
+    were written by tests/tools/oracle_energy_golden.py, which calls only
     oracle/, from the same seeded bytes (checked by digest).
       (i)   |E_gpu - E_oracle| / E_oracle at the final iteration <= 1% wherever
             the oracle's own 1-ulp floor (ensemble spread) is below 1%;

@@ -1,6 +1,6 @@
 """Debug: one-batch / one-iteration parity errors per config, repeated."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import oracle
 from blgen import build_config

@@ -3,14 +3,14 @@ energy must match within 1% relative") with the chaos floor beside it, on one
 config: the GPU's energy trace vs the fp64 oracle's, and the oracle from
 1-ulp-perturbed inputs.  Slow on purpose (the C5 oracle is ~3.4e12 fp64 pair
 evaluations per run).
-  python scripts/full_run_energy.py --config C5 [--no-perturbed]"""
+  python tests/tools/full_run_energy.py --config C5 [--no-perturbed]"""
 import argparse
 import json
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import oracle  # noqa: E402

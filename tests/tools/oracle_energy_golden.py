@@ -5,7 +5,7 @@ fp32 oracle -- for the -m gpu full-run energy tests, which are too long to
 recompute on the GPU box's host at test time.
 
 Calls only oracle/ and blgen/ (test infrastructure; no CUDA path).
-Usage: python scripts/oracle_energy_golden.py C4 [--members 12] [--threads 0]
+Usage: python tests/tools/oracle_energy_golden.py C4 [--members 12] [--threads 0]
 """
 import argparse
 import hashlib
@@ -16,7 +16,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
@@ -68,7 +68,7 @@ def main():
     out = {
         "what": f"oracle energy traces for {args.config} (fp64 unperturbed, {args.members} "
                 "fp64 runs from 1-ulp-perturbed xy0, fp32 oracle); written by "
-                "scripts/oracle_energy_golden.py (calls only oracle/)",
+                "tests/tools/oracle_energy_golden.py (calls only oracle/)",
         "config": args.config, "n": g.n, "nnz": int(g.nnz), "batch": cfg.batch, "iters": iters,
         "input_sha256": input_digest(g, xy0), "perturbation_seed": 0,
         "oracle_f64": E.tolist(), "ensemble_f64": ens, "oracle_f32": E32.tolist(),

@@ -10,7 +10,7 @@ the fp64 oracle on the same seeded bytes), written as one JSON document:
   chaos_floor    the oracle's own spread at that iteration: the same run from
                  1-ulp-perturbed inputs, and the fp32 oracle vs the fp64 one
 
-  python scripts/parity_report.py [--configs C1,C2,...] > report.json
+  python tests/tools/parity_report.py [--configs C1,C2,...] > report.json
 """
 import argparse
 import json
@@ -18,7 +18,7 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import oracle  # noqa: E402
