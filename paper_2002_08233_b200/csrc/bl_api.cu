@@ -347,7 +347,11 @@ extern "C" void bl_destroy(bl_ctx *h) {
   for (cudaEvent_t e : h->m_ev)
     if (e) cudaEventDestroy(e);
   cudaFree(h->d_coo_row);
-  cudaFree(h->d_apart);
+  cudaFree(h->d_la_chunks);
+  cudaFree(h->d_la_lrow);
+  cudaFree(h->d_la_lpart);
+  cudaFree(h->d_la_cls);
+  cudaFree(h->d_la_bar);
   cudaFree(h->d_chk);
   cudaFree(h->d_part_st);
   cudaFree(h->d_pend_st);
@@ -494,9 +498,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     // step a5 alone: the standalone high-occupancy kernels (bl_attr.cuh)
     model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
     if ((s = bl_attr_launch(h, k, st)) != BL_OK) return s;
-    snprintf(h->kname_last, sizeof h->kname_last, "bla_edge_kernel + bla_row_sum_kernel");
+    snprintf(h->kname_last, sizeof h->kname_last, "bla_kernel");
     h->driver_last = "standalone";
-    h->launches = 2;
     return BL_OK;
   }
   k.red_cap = red_cap_for(k.chunk4);

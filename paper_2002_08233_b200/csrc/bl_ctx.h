@@ -22,8 +22,16 @@ struct bl_ctx {
   int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
   std::vector<int> item_ptr;  // host copy (per-batch maxima)
   std::vector<int> rowptr_host;  // host copy of rowptr (entry ranges)
-  int *d_coo_row = nullptr;      // COO row id per CSR entry (a5 alone, EU)
-  float2 *d_apart = nullptr;     // a5 alone: one partial per (lane, row) segment
+  int *d_coo_row = nullptr;      // COO row id per CSR entry (metric helpers)
+  // long-row chunks of the standalone CSR walks (a5 alone, EU; bl_attr.cu)
+  bool la_ready = false;
+  int la_nchunks = 0, la_nlong = 0, la_n1 = 0, la_n2 = 0;
+  struct BLAChunk *d_la_chunks = nullptr;
+  int2 *d_la_lrow = nullptr;
+  float2 *d_la_lpart = nullptr;
+  int *d_la_cls = nullptr;  // class-1 then class-2 vertex lists
+  unsigned *d_la_bar = nullptr;  // grid-barrier counter of bla_kernel (monotone)
+  unsigned la_bar_base = 0;
   int n_items = 0;
   // scratch
   float2 *d_part = nullptr;
@@ -101,7 +109,10 @@ void *bl_bh_kernel_fn();                            // bl_bh.cu
 size_t bl_bh_smem_bytes();
 int bl_bh_threads();
 void *bl_cluster_kernel_fn(int tt, int rmode);      // bl_cluster.cu
-// bl_attr.cu: step a5 alone (bl_forces + BL_ATTRACTION_ONLY), two launches;
-// the COO row ids of the CSR (built once per context, shared with EU)
+// bl_attr.cu: step a5 alone (bl_forces + BL_ATTRACTION_ONLY, one launch), the
+// edge-uniformity passes, the COO row ids of the CSR (metric helpers)
 bl_status bl_attr_launch(bl_ctx *h, const BLKParams &k, cudaStream_t st);
 bl_status bl_coo_rows(bl_ctx *h, cudaStream_t st);
+bl_status bl_eu_launch(bl_ctx *h, const float2 *xy, int blocks, double *part, double *stats,
+                       cudaStream_t st);
+int bl_eu_blocks(const bl_ctx *h);  // grid of the edge-uniformity kernel

@@ -61,25 +61,18 @@ void record_time(bl_ctx *h) {
 extern "C" bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu, void *cuda_stream) {
   if (!h || !d_xy || !eu) return bl_fail(h, BL_EINVAL, "NULL argument");
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  const int nb = 4 * h->num_sms;
+  const int nb = bl_eu_blocks(h);
   DevBuf part, stats;
-  BLM_ALLOC(h, S_EU_PART, part, sizeof(double2) * nb);
+  BLM_ALLOC(h, S_EU_PART, part, sizeof(double) * 3 * nb);
   BLM_ALLOC(h, S_EU_STATS, stats, sizeof(double) * 8);
   const float2 *xy = reinterpret_cast<const float2 *>(d_xy);
-  DevBuf row;
-  const bool fresh = h->d_coo_row == nullptr;
-  int launches = 4;
+  const int launches = 1;
   BL_CUDA(h, mark(h, 0, st));
-  if (fresh) {  // once per context: the COO row ids of the CSR entries
-    bl_status s = bl_coo_rows(h, st);
+  // one pass over the rows by degree class with per-lane shifted sums merged
+  // in a fixed order (bla_eu_kernel, bl_attr.cuh; its last block merges)
+  {
+    bl_status s = bl_eu_launch(h, xy, nb, part.as<double>(), stats.as<double>(), st);
     if (s != BL_OK) return s;
-    ++launches;
-  }
-  row.p = h->d_coo_row;
-  for (int pass = 0; pass < 2; ++pass) {
-    blm_eu_pass<<<nb, BLM_NT, 0, st>>>(row.as<int>(), h->d_colidx, xy, (long long)h->nnz, pass,
-                                        stats.as<double>(), part.as<double2>());
-    blm_reduce_parts<<<1, BLM_RT, 0, st>>>(part.as<double2>(), nb, stats.as<double>(), pass);
   }
   BL_CUDA(h, cudaGetLastError());
   BL_CUDA(h, mark(h, 1, st));

@@ -1,8 +1,9 @@
 // bl_metrics.cuh -- the layout quality metrics of §3.7
 // on sm_100a (device side; readings M1-M4 of DESIGN.md §3).
 //
-//   edge uniformity (M2): two passes over the CSR (edges i < j once), fp64
-//     per-thread sums, fixed-order block and grid reductions;
+//   edge uniformity (M2): one entry-parallel pass over the CSR (edges i < j
+//     once; bla_eu_kernel in bl_attr.cuh), fp64 per-lane Welford states
+//     merged in a fixed order;
 //   stress (M1): multi-source BFS, 64 sources per group as one uint64 bitmask
 //     per vertex, pull-based levels inside ONE cooperative kernel (grid barrier
 //     per level); every newly reached (source, vertex) pair at hop distance L
@@ -36,51 +37,8 @@ __device__ __forceinline__ double blm_block_sum(double v, double *sh_warp) {
 }
 
 // ---------------------------------------------------------------- EU (M2)
-// (COO row ids: bla_coo_rows in bl_attr.cuh, built once per context)
-// pass 0: part[b] = (sum of edge lengths, edge count); pass 1: part[b] =
-// sum (l - mu)^2 with mu = stats[0] / stats[1] from pass 0.  Each undirected
-// edge once (entries with j > i).  Entry-parallel, grid-stride with a fixed
-// grid: thread t takes entries t, t + T, t + 2T, ... (8 in flight), so every
-// per-thread sum has a fixed order -> bitwise-reproducible results.
-__global__ void __launch_bounds__(BLM_NT) blm_eu_pass(const int *row, const int *colidx,
-                                                      const float2 *xy, long long nnz, int pass,
-                                                      const double *stats, double2 *part) {
-  __shared__ double sh[BLM_NW];
-  double acc = 0.0, cnt = 0.0;
-  const double mu = pass ? stats[0] / stats[1] : 0.0;
-  const long long T = (long long)gridDim.x * BLM_NT;
-  for (long long k0 = (long long)blockIdx.x * BLM_NT + threadIdx.x; k0 < nnz; k0 += 8 * T) {
-    int ii[8], jj[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const long long k = k0 + u * T;
-      ii[u] = k < nnz ? __ldg(row + k) : 0;
-      jj[u] = k < nnz ? __ldg(colidx + k) : 0;
-    }
-    float2 ci[8], cj[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool take = jj[u] > ii[u];
-      ci[u] = take ? __ldg(xy + ii[u]) : make_float2(0.f, 0.f);
-      cj[u] = take ? __ldg(xy + jj[u]) : make_float2(0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (jj[u] <= ii[u]) continue;
-      const double dx = (double)cj[u].x - (double)ci[u].x, dy = (double)cj[u].y - (double)ci[u].y;
-      const double l = sqrt(dx * dx + dy * dy);
-      if (pass) {
-        acc += (l - mu) * (l - mu);
-      } else {
-        acc += l;
-        cnt += 1.0;
-      }
-    }
-  }
-  const double s = blm_block_sum(acc, sh);
-  const double c = blm_block_sum(cnt, sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = make_double2(s, c);
-}
+// One entry-parallel pass with per-lane Welford states (bla_eu_kernel and
+// bla_eu_final in bl_attr.cuh).
 
 // Fixed-order sum of x[0..count) by ONE block of BLM_RT threads: thread t
 // sums x[t], x[t + BLM_RT], ... in order, then a fixed pairwise tree in
