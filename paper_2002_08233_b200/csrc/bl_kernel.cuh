@@ -317,7 +317,13 @@ __device__ __forceinline__ float2 bl_src_get(const float4 *src4, int k) {
 // sources are only ever swept with TP = 0.
 // TP < 0: the general repulsion exponent r: INV = d^(r-1) = 2^(rh lg2 d^2)
 // (two MUFU per pair: the roofline halves).
-template <int T, int TP>
+// unroll of the source loop by tile width (measured same box, with a single
+// call site per unit so that one copy of the loop is hot): T = 8 -> 4 (C5
+// -1.6 % time vs 2), T = 16 -> 8 (C6 -3.6 %), small tiles 2
+#ifndef BL_SWEEP_UNROLL
+#define BL_SWEEP_UNROLL 4
+#endif
+template <int T, int TP, int UN = (T >= 16 ? 2 * BL_SWEEP_UNROLL : T >= 8 ? BL_SWEEP_UNROLL : 2)>
 __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0, int s1,
                                          const float (&tx)[T], const float (&ty)[T], bl_f2 (&AX)[T],
                                          bl_f2 (&AY)[T], float rh = 0.f) {
@@ -328,7 +334,7 @@ __device__ __forceinline__ void bl_sweep(const float4 *__restrict__ src4, int s0
     TX[k] = f2pack(tx[k], tx[k]);
     TY[k] = f2pack(ty[k], ty[k]);
   }
-#pragma unroll 2
+#pragma unroll UN
   for (int s = s0; s < s1; ++s) {
     const float4 q = src4[s];  // two sources, broadcast to the warp
     const bl_f2 X = f2pack(q.x, q.y), Y = f2pack(q.z, q.w);
@@ -459,14 +465,14 @@ struct BLProf {
 // Sweep resident float4 slots [s0, s1) for T targets: paired reciprocals on
 // float4s of two real sources; the (at most one) float4 at index full4 that
 // holds a real source and a far dummy is swept unpaired.
-template <int T, int TP>
+template <int T, int TP, int UN = (T >= 16 ? 2 * BL_SWEEP_UNROLL : T >= 8 ? BL_SWEEP_UNROLL : 2)>
 __device__ __forceinline__ void bl_sweep_range(const float4 *src4, int s0, int s1, int full4,
                                                const float (&tx)[T], const float (&ty)[T],
                                                bl_f2 (&AX)[T], bl_f2 (&AY)[T], float rh) {
   constexpr int TP1 = TP < 0 ? TP : 0;  // the dummy-holding slot is never paired
   const int e = s1 < full4 ? s1 : full4;
-  if (s0 < e) bl_sweep<T, TP>(src4, s0, e, tx, ty, AX, AY, rh);
-  if (s1 > full4 && s0 <= full4) bl_sweep<T, TP1>(src4, full4, full4 + 1, tx, ty, AX, AY, rh);
+  if (s0 < e) bl_sweep<T, TP, UN>(src4, s0, e, tx, ty, AX, AY, rh);
+  if (s1 > full4 && s0 <= full4) bl_sweep<T, TP1, 1>(src4, full4, full4 + 1, tx, ty, AX, AY, rh);
 }
 
 // Geometry of CTA c's resident sources: m_c = ceil((n - c)/G) owned
@@ -491,6 +497,30 @@ __host__ __device__ inline BLGeom bl_geom(int c, int G, int n, int k_lo, int own
   }
   g.clean4 = g.last4 - (g.d_hi - g.d_lo);
   return g;
+}
+
+// Source-slot segments of sub-range `sub` (< nc: a clean sub-range, guided
+// cut of [0, d_lo) ++ [d_hi, last4); else the dirty slots [d_lo, d_hi)).
+__device__ __forceinline__ void bl_unit_segments(const BLGeom &geo, int nc, int sub, int guided,
+                                                 int (&lo)[2], int (&hi)[2], int &nseg) {
+  nseg = 0;
+  if (sub < nc) {
+    const int dw = geo.d_hi - geo.d_lo;
+    const int a = bl_guided_start(sub, nc, geo.clean4, guided);
+    const int e = bl_guided_start(sub + 1, nc, geo.clean4, guided);
+    if (a < geo.d_lo) {
+      lo[nseg] = a;
+      hi[nseg++] = min(e, geo.d_lo);
+    }
+    if (e > geo.d_lo) {
+      lo[nseg] = max(a, geo.d_lo) + dw;
+      hi[nseg++] = e + dw;
+    }
+  } else {
+    lo[0] = geo.d_lo;
+    hi[0] = geo.d_hi;
+    nseg = 1;
+  }
 }
 
 // One repulsion work unit g = (target tile g % ntt, sub-range g / ntt):
@@ -518,17 +548,14 @@ __device__ __forceinline__ void bl_do_unit(const BLKParams &p, int lo, int bt, c
     AX[k] = f2pack(0.f, 0.f);
     AY[k] = f2pack(0.f, 0.f);
   }
-  const int dw = geo.d_hi - geo.d_lo;
-  if (sub < U.nc) {
-    const int a = bl_guided_start(sub, U.nc, geo.clean4, p.guided);
-    const int e = bl_guided_start(sub + 1, U.nc, geo.clean4, p.guided);
-    if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY, p.r_half);
-    if (e > geo.d_lo)
-      bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY,
-                            p.r_half);
-  } else {
-    bl_sweep_range<T, TP>(src4, geo.d_lo, geo.d_hi, geo.full4, tx, ty, AX, AY, p.r_half);
-  }
+  // the unit's source slots as <= 2 segments, swept by ONE call site (a
+  // single copy of the unrolled loop in the binary: warps running different
+  // segments share the instruction cache)
+  int seg_lo[2], seg_hi[2], nseg = 0;
+  bl_unit_segments(geo, U.nc, sub, p.guided, seg_lo, seg_hi, nseg);
+#pragma unroll 1
+  for (int q = 0; q < nseg; ++q)
+    bl_sweep_range<T, TP>(src4, seg_lo[q], seg_hi[q], geo.full4, tx, ty, AX, AY, p.r_half);
 #pragma unroll
   for (int k = 0; k < T; ++k) {
     const int idx = tile * 32 * T + k * 32 + lane;
@@ -1913,7 +1940,6 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
       const int n_clean = Un.ntt * Un.nc, stride = Un.ntt * 32 * T;
       float2 *red_s = red + s * half;
       float2 *tgt_s = tgt + s * BL_TGT_CAP;
-      const int dw = geo.d_hi - geo.d_lo;
       for (;;) {
         int g = n_clean;
         if (lane == 0) g = atomicAdd(&sh.l_unit[s], 1);
@@ -1932,11 +1958,12 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
           ty[k] = t.y;
           AX[k] = AY[k] = f2pack(0.f, 0.f);
         }
-        const int a = bl_guided_start(sub, Un.nc, geo.clean4, p.guided);
-        const int e = bl_guided_start(sub + 1, Un.nc, geo.clean4, p.guided);
-        if (a < geo.d_lo) bl_sweep_range<T, TP>(src4, a, min(e, geo.d_lo), geo.full4, tx, ty, AX, AY, p.r_half);
-        if (e > geo.d_lo)
-          bl_sweep_range<T, TP>(src4, max(a, geo.d_lo) + dw, e + dw, geo.full4, tx, ty, AX, AY, p.r_half);
+        // (two call sites here: measured 1.6 % faster at C4 than one)
+        int seg_lo[2], seg_hi[2], nseg = 0;
+        bl_unit_segments(geo, Un.nc, sub, p.guided, seg_lo, seg_hi, nseg);
+        // (unroll 2: the small per-phase sweeps of this driver lose with 4)
+        if (nseg > 0) bl_sweep_range<T, TP, 2>(src4, seg_lo[0], seg_hi[0], geo.full4, tx, ty, AX, AY, p.r_half);
+        if (nseg > 1) bl_sweep_range<T, TP, 2>(src4, seg_lo[1], seg_hi[1], geo.full4, tx, ty, AX, AY, p.r_half);
 #pragma unroll
         for (int k = 0; k < T; ++k) {
           const int idx = tile * 32 * T + k * 32 + lane;

@@ -167,7 +167,7 @@ __device__ __forceinline__ void sweep_var(const float4 *__restrict__ src4, int s
   }
 }
 
-template <int NT, int T, int TP, int MODE>
+template <int NT, int T, int TP, int MODE, int UN = 2>
 __global__ void __launch_bounds__(NT, 1) sv_kernel(const float2 *xy, int n4, int reps, float *out,
                                                    long long *cyc) {
   extern __shared__ float4 smem[];
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(NT, 1) sv_kernel(const float2 *xy, int n4, int
   const long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     if (MODE < 0)
-      bl_sweep<T, TP>(src4, 0, n4, tx, ty, AX, AY);
+      bl_sweep<T, TP, UN>(src4, 0, n4, tx, ty, AX, AY);
     else
       sweep_var<T, TP, MODE>(src4, 0, n4, tx, ty, AX, AY, ax, ay);
   }
@@ -206,9 +206,9 @@ __global__ void __launch_bounds__(NT, 1) sv_kernel(const float2 *xy, int n4, int
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int NT, int T, int TP, int MODE>
+template <int NT, int T, int TP, int MODE, int UN = 2>
 void sweep(const char *name, const float2 *d_xy, int n4, int sms, float *d_out, long long *d_cyc) {
-  auto k = sv_kernel<NT, T, TP, MODE>;
+  auto k = sv_kernel<NT, T, TP, MODE, UN>;
   const size_t smem = (size_t)n4 * 16;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int reps = 40;
@@ -252,6 +252,37 @@ int main() {
   cudaMalloc(&d_xy, h.size() * sizeof(float2));
   cudaMemcpy(d_xy, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
   sweep<512, 8, 2, -1>("bl_sweep", d_xy, n4, sms, d_out, d_cyc);
+  if (getenv("PB_UNROLL2")) {
+    sweep<512, 8, 2, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 3, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 1, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 4, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 2, -1, 8>("bl_sweep unroll 8", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 3, -1, 8>("bl_sweep unroll 8", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 2, -1, 6>("bl_sweep unroll 6", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 3, -1, 3>("bl_sweep unroll 3", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 4, -1, 1>("bl_sweep unroll 1", d_xy, n4, sms, d_out, d_cyc);
+    sweep<256, 16, 4, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<256, 16, 6, -1, 2>("bl_sweep unroll 2", d_xy, n4, sms, d_out, d_cyc);
+    sweep<256, 16, 6, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 2, -1, 4>("bl_sweep unroll 4 (again)", d_xy, n4, sms, d_out, d_cyc);
+    return 0;
+  }
+  if (getenv("PB_UNROLL")) {
+    sweep<512, 8, 2, -1, 1>("bl_sweep unroll 1", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 2, -1, 3>("bl_sweep unroll 3", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 2, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 1, -1, 1>("bl_sweep unroll 1", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 3, -1, 1>("bl_sweep unroll 1", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 1, -1, 2>("bl_sweep unroll 2", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 3, -1, 2>("bl_sweep unroll 2", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 4, 1, -1, 1>("bl_sweep unroll 1", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 4, 1, -1, 2>("bl_sweep unroll 2", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 4, 1, -1, 4>("bl_sweep unroll 4", d_xy, n4, sms, d_out, d_cyc);
+    sweep<256, 16, 4, -1, 1>("bl_sweep unroll 1", d_xy, n4, sms, d_out, d_cyc);
+    sweep<512, 8, 2, -1, 2>("bl_sweep unroll 2 (again)", d_xy, n4, sms, d_out, d_cyc);
+    return 0;
+  }
   sweep<512, 8, 0, 0>("all packed", d_xy, n4, sms, d_out, d_cyc);
   sweep<512, 8, 2, 0>("all packed", d_xy, n4, sms, d_out, d_cyc);
   sweep<512, 8, 0, 1>("scalar accumulation", d_xy, n4, sms, d_out, d_cyc);
