@@ -729,10 +729,7 @@ def test_full_run_energy_vs_oracle_golden(name):
       (iii) the horizon: E_gpu(t) within 1% of E_oracle(t) for every t up to
             the last iteration where the floor is <= 0.1%;
       (iv)  E_gpu(final) inside [ensemble min - 1%, ensemble max + 1%]."""
-    import sys
-    sys.path.insert(0, __import__("os").path.join(__import__("os").path.dirname(__file__), "..",
-                                                  "scripts"))
-    from oracle_energy_golden import input_digest
+    from tests.tools.oracle_energy_golden import input_digest
     gold = _golden_energy(name)
     g, xy0, cfg = build_config(name)
     assert gold["input_sha256"] == input_digest(g, xy0), "golden inputs differ from blgen's"
