@@ -415,7 +415,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   bl_status s;
   const bool attr_only = forces_mode && (p->flags & BL_ATTRACTION_ONLY);
   if (!attr_only && (s = grow(h, h->d_part, h->part_cap, (size_t)3 * b * G)) != BL_OK) return s;
-  if ((s = grow(h, h->d_pend, h->pend_cap, (size_t)3 * b)) != BL_OK) return s;
+  if ((s = grow(h, h->d_pend, h->pend_cap, (size_t)2 * b)) != BL_OK) return s;
   const int mi = forces_mode ? max_items_per_batch(h, b, first, count)
                              : max_items_per_batch(h, b, 0, n);
   if ((s = grow(h, h->d_attr, h->attr_cap, (size_t)mi)) != BL_OK) return s;
@@ -454,7 +454,6 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.item_k0 = h->d_item_k0;
   k.part = h->d_part;
   k.pend = h->d_pend;
-  k.pend_nbuf = 2;
   // one barrier per batch needs >= 4 batches per iteration,
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
@@ -554,7 +553,6 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     if (lat_ok && (lat_env == 1 || lat_auto)) {
       k.pipelined = 3;
       k.part_nbuf = 2;
-      k.pend_nbuf = 3;  // batch q-2's coordinates read before barrier q-1 (bl_lat_pre)
       k.red_cap = red_lat;
       k.guided = env_int("BL_GUIDED", 1);
       k.nsub_max = std::max(2, env_int("BL_NSUB", 6));
@@ -568,7 +566,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
       return bl_fail(h, BL_ENOMEM, "checked-build buffers");
   }
   if ((s = grow(h, h->d_part_st, h->part_st_cap, (size_t)3 * b * G)) != BL_OK) return s;
-  if ((s = grow(h, h->d_pend_st, h->pend_st_cap, (size_t)3 * b)) != BL_OK) return s;
+  if ((s = grow(h, h->d_pend_st, h->pend_st_cap, (size_t)2 * b)) != BL_OK) return s;
   BL_CUDA(h, cudaMemsetAsync(h->d_chk, 0, sizeof(unsigned) * 8, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_xy_st, 0, sizeof(unsigned) * (size_t)n, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_part_st, 0, sizeof(unsigned) * h->part_st_cap, st));

@@ -124,8 +124,7 @@ struct BLKParams {
   const int *rowptr, *colidx;
   const int *item_ptr, *item_v, *item_k0;
   float2 *part;          // [2][b][G] (pipelined path double-buffers by batch parity)
-  float2 *pend;          // [pend_nbuf][b] new coordinates of the last batches
-  int pend_nbuf;         // 2 (pipelined / async), 3 (latency driver: batch q-2 read early)
+  float2 *pend;          // [2][b]   new coordinates of the last two batches (pipelined)
   int pipelined;         // 1: one grid barrier per batch (needs nb >= 4); 2: the same
                          // without CTA-wide barriers between phases (bl_run_async)
   int part_nbuf;         // part buffers (2: pipelined, 3: async)
@@ -1032,7 +1031,7 @@ __device__ __forceinline__ double bl_energy_sum_warp(const BLKParams &p, int it)
 __device__ __forceinline__ void bl_chk_nb(const BLKParams &p, int q, int j, int plo, int phi) {
 #ifdef BL_CHECKED
   if (j >= plo && j < phi) {
-    BL_CHK(__ldcg(p.pend_st + (size_t)((q - 1) % p.pend_nbuf) * p.b + (j - plo)) == (unsigned)q,
+    BL_CHK(__ldcg(p.pend_st + (size_t)((q - 1) & 1) * p.b + (j - plo)) == (unsigned)q,
            BLC_PEND_STAMP, q, j);
   } else {
     BL_CHK(__ldcg(p.xy_st + j) == bl_exp_stamp(p, j, q - 2), BLC_XY_STAMP, q, j);
@@ -1041,20 +1040,15 @@ __device__ __forceinline__ void bl_chk_nb(const BLKParams &p, int q, int j, int 
 }
 
 // Update of one owned vertex v of batch q (warp-cooperative); ||f||^2 -> *eq.
-// pre = true (latency driver, rows of > 32 entries): the lane's attraction
-// over every neighbour NOT in batch q-1 was summed before the barrier into
-// (psx, psy) (bl_lat_pre); the batch-(q-1) neighbours are stash[0..nstash).
 __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, double stepd,
                                               float4 *src4, double *eq, const int *srow,
-                                              int sdeg, bool pre = false, float psx = 0.f,
-                                              float psy = 0.f, const int *stash = nullptr,
-                                              int nstash = 0) {
+                                              int sdeg) {
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b;
   const int local = v - lo;
   // neighbours in batch q-1 are read from pend (committed only next phase)
   int plo = 0, phi = 0;
-  const float2 *pend_prev = p.pend + (size_t)((q + p.pend_nbuf - 1) % p.pend_nbuf) * p.b;
+  const float2 *pend_prev = p.pend + (size_t)((q - 1) & 1) * p.b;
   if (q >= 1) {
     plo = ((q - 1) % p.nb) * p.b;
     phi = min(plo + p.b, p.n);
@@ -1071,20 +1065,9 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     cj_st = (j_st >= plo && j_st < phi) ? __ldcg(pend_prev + (j_st - plo)) : __ldcg(p.xy + j_st);
   }
   int k0 = 0, k1 = 0;
-  if (!srow && !pre) {
+  if (!srow) {
     k0 = __ldg(p.rowptr + v);
     k1 = __ldg(p.rowptr + v + 1);
-  }
-  // pre: the batch-(q-1) neighbours' coordinates, issued with the partials
-  int js[4];
-  float2 cs[4];
-  if (pre) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = lane + 32 * u;
-      js[u] = i < nstash ? stash[i] : -1;
-      cs[u] = js[u] >= 0 ? __ldcg(pend_prev + (js[u] - plo)) : ci;
-    }
   }
   float rx = 0.f, ry = 0.f;
   {
@@ -1173,29 +1156,8 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       }
     }
   };
-  if (pre) {
-    sx = psx;
-    sy = psy;
-    auto stash_terms = [&](auto fast) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (js[u] < 0) continue;
-        if (BL_CHK_ON) bl_chk_nb(p, q, js[u], plo, phi);
-        const float dx = cs[u].x - ci.x, dy = cs[u].y - ci.y;
-        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
-        const float rs = bl_rsqrt(d2);
-        const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
-        sx = fmaf(coef, dx, sx);
-        sy = fmaf(coef, dy, sy);
-      }
-    };
-    if (p.amode == 0 && p.rmode == 0) stash_terms(std::true_type{});
-    else stash_terms(std::false_type{});
-  } else if (p.amode == 0 && p.rmode == 0) {
-    scan_row(std::true_type{});  // branch hoisted out of the loop
-  } else {
-    scan_row(std::false_type{});
-  }
+  if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});  // branch hoisted out of the loop
+  else scan_row(std::false_type{});
   rx = bl_warp_sum0(rx);
   ry = bl_warp_sum0(ry);
   sx = bl_warp_sum0(sx);
@@ -1211,10 +1173,10 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       cv.y = (float)((double)cv.y + sc * fy);
       bl_src_set(src4, (v - c) / G, cv);
     }
-    p.pend[(size_t)(q % p.pend_nbuf) * p.b + local] = cv;
+    p.pend[(size_t)(q & 1) * p.b + local] = cv;
     if (BL_CHK_ON) {
       BL_CHK(local >= 0 && local < p.b, BLC_BOUNDS, 3, local);
-      p.pend_st[(size_t)(q % p.pend_nbuf) * p.b + local] = (unsigned)q + 1u;
+      p.pend_st[(size_t)(q & 1) * p.b + local] = (unsigned)q + 1u;
     }
     *eq = qq;
   }
@@ -1922,86 +1884,6 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
 //             every target in fixed order -> part, arrives at barrier q.
 // Same values and summation order as the asynchronous driver's (the clean
 // sub-ranges in order, then the dirty one).  Needs nb >= 4.
-// Latency driver, before barrier Q (member v of batch Q, rows of > 32
-// entries): the lane's attraction sum over every neighbour NOT in batch Q-1,
-// whose coordinates are already final and visible after barrier Q-1 -- batch
-// Q-2's in pend[(Q-2) % 3] (written before arrival Q-1), all others committed
-// in xy (batch <= Q-3, committed before arrival Q-1; batch Q itself and later
-// ones from the previous iteration).  Batch Q-1's neighbours (a contiguous
-// range of the sorted row) go to stash[] for after the barrier.  Returns
-// false (and the update takes the plain path) if they overflow BL_LAT_STASH.
-#define BL_LAT_STASH 128
-__device__ __forceinline__ bool bl_lat_pre(const BLKParams &p, int Q, float2 ci, int k0, int k1,
-                                           int *stash, int &nstash, float &psx, float &psy) {
-  const int lane = threadIdx.x & 31, nb = p.nb;
-  int plo1 = 0, phi1 = 0, plo2 = 0, phi2 = 0;
-  if (Q >= 1) {
-    plo1 = ((Q - 1) % nb) * p.b;
-    phi1 = min(plo1 + p.b, p.n);
-  }
-  if (Q >= 2) {
-    plo2 = ((Q - 2) % nb) * p.b;
-    phi2 = min(plo2 + p.b, p.n);
-  }
-  const float2 *pend2 = p.pend + (size_t)((Q + p.pend_nbuf - 2) % p.pend_nbuf) * p.b;
-  const float rep = (p.flags & 1u) ? 0.f : p.ck2;
-  const unsigned lt = (1u << lane) - 1u;
-  float sx = 0.f, sy = 0.f;
-  int nst = 0;
-  for (int base = k0; base < k1; base += 256) {
-    int jj[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = base + lane + 32 * u;
-      jj[u] = k < k1 ? __ldg(p.colidx + k) : -1;
-    }
-    float2 cj[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int j = jj[u];
-      const bool post = j >= plo1 && j < phi1;
-      const unsigned m = __ballot_sync(0xffffffffu, post);
-      if (post) {
-        const int pos = nst + __popc(m & lt);
-        if (pos < BL_LAT_STASH) stash[pos] = j;
-      }
-      nst += __popc(m);
-      if (post) jj[u] = -1;
-      cj[u] = jj[u] < 0 ? ci : (jj[u] >= plo2 && jj[u] < phi2) ? __ldcg(pend2 + (jj[u] - plo2))
-                                                                : __ldcg(p.xy + jj[u]);
-#ifdef BL_CHECKED
-      if (jj[u] >= 0) {
-        if (jj[u] >= plo2 && jj[u] < phi2)
-          BL_CHK(__ldcg(p.pend_st + (size_t)((Q + p.pend_nbuf - 2) % p.pend_nbuf) * p.b + (jj[u] - plo2)) ==
-                     (unsigned)(Q - 1),
-                 BLC_PEND_STAMP, Q, jj[u]);
-        else
-          BL_CHK(__ldcg(p.xy_st + jj[u]) == bl_exp_stamp(p, jj[u], Q - 3), BLC_XY_STAMP, Q, jj[u]);
-      }
-#endif
-    }
-    auto terms = [&](auto fast) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (jj[u] < 0) continue;
-        const float dx = cj[u].x - ci.x, dy = cj[u].y - ci.y;
-        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
-        const float rs = bl_rsqrt(d2);
-        const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
-        sx = fmaf(coef, dx, sx);
-        sy = fmaf(coef, dy, sy);
-      }
-    };
-    if (p.amode == 0 && p.rmode == 0) terms(std::true_type{});
-    else terms(std::false_type{});
-  }
-  __syncwarp();
-  nstash = nst;
-  psx = sx;
-  psy = sy;
-  return nst <= BL_LAT_STASH;
-}
-
 template <int T, int TP>
 __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, float2 *tgt,
                                            float2 *red, BLShared &sh) {
@@ -2157,23 +2039,13 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
     long long t_det = 0;
 #endif
     if (q >= 1) {
-      // this warp's member before the barrier: a row of <= 32 entries is
-      // staged; a longer one gets its attraction over every neighbour not in
-      // batch q-2 summed now (bl_lat_pre), the rest after the barrier
-      int deg = -1, nst = 0;
-      bool pre = false;
-      float psx = 0.f, psy = 0.f;
-      int *stash = &sh.rows[1][0][0] + warp * BL_LAT_STASH;
+      // this warp's member: its CSR row (constant) before the barrier
+      int deg = -1;
       if (warp < m) {
         const int v = v0 + warp * G;
         const int k0 = __ldg(p.rowptr + v);
         deg = __ldg(p.rowptr + v + 1) - k0;
-        if (deg <= 32) {
-          if (lane < deg) myrow[lane] = __ldg(p.colidx + k0 + lane);
-        } else {
-          pre = bl_lat_pre(p, q - 1, bl_src_get(src4, (v - c) / G), k0, k0 + deg, stash, nst, psx,
-                           psy);
-        }
+        if (deg <= 32 && lane < deg) myrow[lane] = __ldg(p.colidx + k0 + lane);
         __syncwarp();
       }
       if (warp == 0) {
@@ -2207,7 +2079,7 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
       bl_jitter(p, 32);
       if (vs.stop_flag == 0 && warp < m)
         bl_update_one(p, q - 1, v0 + warp * G, step_u, src4, &sh.e_task[warp],
-                      deg <= 32 ? myrow : nullptr, deg <= 32 ? deg : 0, pre, psx, psy, stash, nst);
+                      deg <= 32 ? myrow : nullptr, deg <= 32 ? deg : 0);
     }
     ubar();  // every member of M(q-1) updated (src4, pend, e_task)
 #ifdef BL_PHASE_TS
