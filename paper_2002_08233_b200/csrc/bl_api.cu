@@ -27,7 +27,7 @@
 #define BL_DEFAULT_T 8
 #endif
 #ifndef BL_DEFAULT_TP
-#define BL_DEFAULT_TP 2
+#define BL_DEFAULT_TP 1
 #endif
 
 static thread_local std::string g_create_err;
@@ -458,22 +458,20 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // targets within the staging buffer, an even batch and 16-byte aligned
   // coordinates (16-byte cp.async of target pairs)
   // kernel variant: r != -1 -> <512,8,-1> (two MUFU per pair);
-  // very large batches (b n >= 5e8, e.g. 2^20 vertices x 1024) -> <256,16,6>
-  // (fewer, wider warps amortise best); latency-bound batches (b <= 512 and
+  // latency-bound batches (b <= 512 and
   // b n <= BL_SMALL_PAIRS, default 2^24) -> <512,2,1>: 64-target tiles and
   // >= 4-slot sub-ranges spread each batch's small sweep over all 16 warps
   // instead of a few long units (measured: C2 -17 %, C3 b=256 -29 %, C4 -23 %
-  // per batch vs <512,8,2>; C3 b=1024 +34 %: its 16 tiles keep <512,8,2>);
-  // else <512,8,2>.  BL_NT / BL_T / BL_TP (read at bl_create)
-  // pin a variant.
+  // per batch vs <512,8,2>; C3 b=1024 +34 %: its 16 tiles keep the wide one);
+  // else <512,8,1> (round 2, with the unroll-4 sweep, same box: C5 -1.9 %,
+  // C6 -3.3 % time vs <512,8,2>; C6 used <256,16,6> before, now 3.3 % slower
+  // than <512,8,1>).  BL_NT / BL_T / BL_TP (read at bl_create) pin a variant.
   model_codes(p, &k.amode, &k.rmode, &k.a_half, &k.r_half);
   const long long bn = (long long)b * n;
   const bool user_variant = getenv("BL_NT") || getenv("BL_T") || getenv("BL_TP");
-  const bool wide = !user_variant && bn >= 500000000LL;
   const bool small_b = !user_variant && b <= 512 &&
                        bn <= (long long)env_int("BL_SMALL_PAIRS", 1 << 24);
   const BLVariant *vt = k.rmode != 0 ? find_variant(512, 8, -1)
-                        : wide && !attr_only ? find_variant(256, 16, 6)
                         : small_b && !attr_only ? find_variant(512, 2, 1)
                                               : find_variant(h->NT, h->T, h->TP);
   // batch randomisation (readings R1-R2): the two-barrier driver (its phase U
@@ -523,8 +521,9 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
     // fewer, flatter units than the pipelined driver's tail-minimising
     // quadratic profile: with no phase-end barrier the tail is overlapped, and
     // each unit's overhead (target loads, partial stores, combine) counts
-    // (measured at C5: 6 sub-ranges, linear profile 0.90 vs 8 quadratic 0.88)
-    k.guided = env_int("BL_GUIDED", 1);
+    // (measured at C5: 6 sub-ranges, linear profile 0.90 vs 8 quadratic 0.88;
+    // round 2 with <512,8,1>: equal sizes 0.2 % faster than linear)
+    k.guided = env_int("BL_GUIDED", 0);
     k.nsub_max = std::max(2, env_int("BL_NSUB", 6));
     k.spin_max = (unsigned)std::max(32, env_int("BL_SPIN", 512));
     k.afence_gpu = env_int("BL_AFENCE", 0);

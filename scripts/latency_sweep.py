@@ -25,7 +25,7 @@ import paper_2002_08233_b200 as bl  # noqa: E402
 from blgen import build_config  # noqa: E402
 
 KNOBS = {"T": "BL_T", "TP": "BL_TP", "NT": "BL_NT", "MU": "BL_MIN_UNIT4", "ASYNC": "BL_ASYNC",
-         "NSUB": "BL_NSUB", "SPIN": "BL_SPIN", "CLUSTER": "BL_CLUSTER", "PIPE": "BL_PIPELINE", "LAT": "BL_LAT"}
+         "NSUB": "BL_NSUB", "SPIN": "BL_SPIN", "CLUSTER": "BL_CLUSTER", "PIPE": "BL_PIPELINE", "LAT": "BL_LAT", "GUIDED": "BL_GUIDED"}
 
 
 def parse(v):

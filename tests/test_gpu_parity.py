@@ -577,7 +577,7 @@ def test_driver_selection_C5(env, expect, monkeypatch):
         lay.layout_device(d, iters=1, batch=cfg.batch, max_batches=1)
         torch.cuda.synchronize()
         assert bl.bl_driver_name(lay.h) == expect
-        assert bl.bl_kernel_name(lay.h) == "bl_layout_kernel<512,8,2>"
+        assert bl.bl_kernel_name(lay.h) == "bl_layout_kernel<512,8,1>"
 
 
 @pytest.mark.parametrize("flags", [0, 1])
