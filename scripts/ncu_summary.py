@@ -46,7 +46,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("csv")
     ap.add_argument("--workload", default="C5")
-    ap.add_argument("--kernel", default="bl_layout_kernel<512,8,2>")
+    ap.add_argument("--kernel", default="bl_layout_kernel<512,8,1>")
     a = ap.parse_args()
     m = read(a.csv)
     src = (f"ncu --set full --clock-control none of scripts/profile_run.py --config {a.workload} "
