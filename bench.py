@@ -509,11 +509,14 @@ def bench_metrics(lay, d_xy, g, peaks, sm_mhz, nsm, stream, sources=1024):
     """Secondary object: the §3.7 quality metrics on the bench's
     final layout, each with a stated roofline fraction:
       EU: 2 passes x (4 nnz + 4 (n+1) + 8 n) algorithmic bytes vs HBM;
-      stress: bit-parallel BFS (64 sources per word) -- bytes = 12 B per CSR
-        entry examined + 24 B per vertex per level (visited, next, rowptr) vs
-        HBM, and TEPS (sources x nnz / t, the Graph500 convention);
-      NP: ~5 (n-1) squared-distance evaluations per query (4 radix-select
-        passes + the tie count), 5 FP32 ops each, vs the FP32 lane peak.
+      stress: bit-parallel BFS (256 sources per 256-bit mask) -- bytes =
+        36 B per CSR entry examined (index + mask gather) + 72 B per vertex
+        per level (visited, next, rowptr) vs HBM, and TEPS (sources x nnz /
+        t, the Graph500 convention);
+      NP: the brute-force definition's n - 1 squared-distance evaluations per
+        query (the one-scan threshold kernels do exactly that for deg <= 256;
+        the radix select of the few larger queries does ~5 scans), 5 FP32
+        lane-ops each, vs the FP32 lane peak.
     Timed with CUDA events around the (synchronous) C-ABI calls, after one
     warm-up call (the scratch is allocated once per context)."""
     import torch
@@ -540,9 +543,9 @@ def bench_metrics(lay, d_xy, g, peaks, sm_mhz, nsm, stream, sources=1024):
     eu_bytes = 2.0 * (4 * g.nnz + 4 * (g.n + 1) + 8 * g.n)
     st, t_st, w_st = timed(lambda: bl.bl_stress(lay.h, d_xy, src, stream), 2)
     levels, examined, _ = bl.bl_debug_counters(lay.h)
-    st_bytes = 12.0 * examined + 24.0 * g.n * levels
+    st_bytes = 36.0 * examined + 72.0 * g.n * levels
     npv, t_np, w_np = timed(lambda: bl.bl_neighborhood_preservation(lay.h, d_xy, None, stream), 2)
-    evals = 5.0 * (g.n - 1) * g.n
+    evals = float(g.n - 1) * g.n
     fp32_evals = nsm * 128 * sm_mhz * 1e6 / 5.0
     return {
         "layout": "the bench's final layout",

@@ -11,6 +11,7 @@
 // in flight.  Every sum has a fixed order: bitwise-reproducible results.
 #pragma once
 #include "bl_kernel.cuh"
+#include "bl_rows.h"
 
 #define BLA_NT 256
 #define BLA_LONG 64     // rows above this many entries are cut into chunks
@@ -23,10 +24,6 @@ __global__ void bla_coo_rows(const int *rowptr, int n, int *row) {
     for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) row[k] = i;
 }
 
-// one long-row chunk: vertex, entry range, index of the long row
-struct BLAChunk {
-  int v, k0, k1, li;
-};
 
 // attraction coefficient x Δ for one entry (reading C15), fp32 as the layout
 template <bool FAST>

@@ -80,8 +80,8 @@ struct bl_ctx {
   size_t part_st_cap = 0, pend_st_cap = 0;
   // quality-metric scratch: grown on first use, kept for the context's life
   // (no allocation inside a metric call after the first)
-  void *m_scr[20] = {nullptr};
-  size_t m_cap[20] = {0};
+  void *m_scr[24] = {nullptr};
+  size_t m_cap[24] = {0};
   long long m_counters[4] = {0, 0, 0, 0};  // bl_debug_counters
   cudaEvent_t m_ev[2] = {nullptr, nullptr};  // GPU time of the last metric call
 };
@@ -113,6 +113,7 @@ void *bl_cluster_kernel_fn(int tt, int rmode);      // bl_cluster.cu
 // edge-uniformity passes, the COO row ids of the CSR (metric helpers)
 bl_status bl_attr_launch(bl_ctx *h, const BLKParams &k, cudaStream_t st);
 bl_status bl_coo_rows(bl_ctx *h, cudaStream_t st);
+bl_status bl_long_rows(bl_ctx *h);  // degree classes of the rows (bl_attr.cu), built once
 bl_status bl_eu_launch(bl_ctx *h, const float2 *xy, int blocks, double *part, double *stats,
                        cudaStream_t st);
 int bl_eu_blocks(const bl_ctx *h);  // grid of the edge-uniformity kernel

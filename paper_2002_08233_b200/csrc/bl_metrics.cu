@@ -22,7 +22,7 @@ struct DevBuf {
 enum {
   S_EU_PART, S_EU_STATS, S_ST_SRC, S_ST_VIS, S_ST_FA, S_ST_FB, S_ST_AA, S_ST_AB, S_ST_AN,
   S_ST_FLAG, S_ST_BAR, S_ST_OUT4, S_ST_OUTN, S_NP_Q, S_NP_JAC, S_NP_OUT, S_NP_CNT, S_EU_ROW,
-  S_ST_WORK
+  S_ST_WORK, S_ST_LMASK, S_NP_SLOTS
 };
 cudaError_t scratch(bl_ctx *h, int slot, size_t bytes, DevBuf &buf) {
   bytes = std::max<size_t>(bytes, 16);
@@ -98,14 +98,20 @@ extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sour
   cudaStream_t st = (cudaStream_t)cuda_stream;
   std::vector<int32_t> src(nsrc);
   for (int32_t t = 0; t < nsrc; ++t) src[t] = sources ? sources[t] : t;
+  {
+    bl_status s = bl_long_rows(h);  // the degree classes (bl_attr.cu)
+    if (s != BL_OK) return s;
+  }
   int occ = 0;
   BL_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blm_stress_kernel, BLM_NT, 0));
   const int G = h->num_sms * std::max(1, std::min(occ, 4));
-  DevBuf d_src, vis, fa, fb, aA, aB, aN, flag, bar, out4, outN;
+  const size_t vb = sizeof(unsigned long long) * BLM_SW * (size_t)n;
+  DevBuf d_src, vis, fa, fb, aA, aB, aN, flag, bar, out4, outN, lmask;
   BLM_ALLOC(h, S_ST_SRC, d_src, sizeof(int32_t) * nsrc);
-  BLM_ALLOC(h, S_ST_VIS, vis, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, S_ST_FA, fa, sizeof(unsigned long long) * n);
-  BLM_ALLOC(h, S_ST_FB, fb, sizeof(unsigned long long) * n);
+  BLM_ALLOC(h, S_ST_VIS, vis, vb);
+  BLM_ALLOC(h, S_ST_FA, fa, vb);
+  BLM_ALLOC(h, S_ST_FB, fb, vb);
+  BLM_ALLOC(h, S_ST_LMASK, lmask, sizeof(unsigned long long) * BLM_SW * (size_t)std::max(1, h->la_nchunks));
   BLM_ALLOC(h, S_ST_AA, aA, sizeof(double) * G * BLM_NT);
   BLM_ALLOC(h, S_ST_AB, aB, sizeof(double) * G * BLM_NT);
   BLM_ALLOC(h, S_ST_AN, aN, sizeof(unsigned long long) * G * BLM_NT);
@@ -127,6 +133,15 @@ extern "C" bl_status bl_stress(bl_ctx *h, const float *d_xy, const int32_t *sour
   k.vis = vis.as<unsigned long long>();
   k.frontA = fa.as<unsigned long long>();
   k.frontB = fb.as<unsigned long long>();
+  k.lmask = lmask.as<unsigned long long>();
+  k.cls1 = h->d_la_cls;
+  k.cls2 = h->d_la_cls + h->la_n1;
+  k.n1 = h->la_n1;
+  k.n2 = h->la_n2;
+  k.nchunks = h->la_nchunks;
+  k.nlong = h->la_nlong;
+  k.chunks = h->d_la_chunks;
+  k.lrow = h->d_la_lrow;
   k.accA = aA.as<double>();
   k.accB = aB.as<double>();
   k.accN = aN.as<unsigned long long>();
@@ -170,18 +185,61 @@ extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
     nq = n;
   }
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  DevBuf d_q, jac, out, cnt;
+  // route each query by kk = min(deg, n - 1): the one-scan threshold kernels
+  // for kk <= 32 (8 queries per warp) and kk <= 256 (two per warp), the radix
+  // select for the rest (bln_np_fast / blm_np_kernel, bl_metrics.cuh)
+  constexpr int K1 = 32, CAP1 = 128, QW1 = 8, K2 = 256, CAP2 = 512, QW2 = 2;
+  std::vector<int32_t> slots(nq);
+  int n1 = 0, n2 = 0, n3 = 0;
+  {
+    std::vector<int32_t> s2, s3;
+    for (int32_t t = 0; t < nq; ++t) {
+      const int i = queries ? queries[t] : t;
+      const int kk = std::min(h->rowptr_host[i + 1] - h->rowptr_host[i], n - 1);
+      if (kk <= K1) slots[n1++] = t;
+      else if (kk <= K2) s2.push_back(t);
+      else s3.push_back(t);
+    }
+    n2 = (int)s2.size();
+    n3 = (int)s3.size();
+    std::copy(s2.begin(), s2.end(), slots.begin() + n1);
+    std::copy(s3.begin(), s3.end(), slots.begin() + n1 + n2);
+  }
+  DevBuf d_q, jac, out, cnt, d_slots;
   if (queries) {
     BLM_ALLOC(h, S_NP_Q, d_q, sizeof(int32_t) * nq);
     BL_CUDA(h, cudaMemcpyAsync(d_q.p, queries, sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st));
   }
+  BLM_ALLOC(h, S_NP_SLOTS, d_slots, sizeof(int32_t) * nq);
+  BL_CUDA(h, cudaMemcpyAsync(d_slots.p, slots.data(), sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st));
   BLM_ALLOC(h, S_NP_JAC, jac, sizeof(double) * nq);
   BLM_ALLOC(h, S_NP_OUT, out, sizeof(double));
   BLM_ALLOC(h, S_NP_CNT, cnt, sizeof(int));
+  const float2 *xy = reinterpret_cast<const float2 *>(d_xy);
+  const int *qp = queries ? d_q.as<int>() : nullptr, *sp = d_slots.as<int>();
+  const size_t sm1 = sizeof(unsigned long long) * (BLN_NT / 32) * QW1 * CAP1;
+  const size_t sm2 = sizeof(unsigned long long) * (BLN_NT / 32) * QW2 * CAP2;
+  BL_CUDA(h, cudaFuncSetAttribute(bln_np_fast<QW1, CAP1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+  BL_CUDA(h, cudaFuncSetAttribute(bln_np_fast<QW2, CAP2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+  int launches = 1;
   BL_CUDA(h, mark(h, 0, st));
-  blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx,
-                                                reinterpret_cast<const float2 *>(d_xy), n,
-                                                queries ? d_q.as<int>() : nullptr, nq, jac.as<double>());
+  if (n1) {
+    const int per = (BLN_NT / 32) * QW1;
+    bln_np_fast<QW1, CAP1><<<(n1 + per - 1) / per, BLN_NT, sm1, st>>>(h->d_rowptr, h->d_colidx, xy, n, qp,
+                                                                     sp, n1, jac.as<double>());
+    ++launches;
+  }
+  if (n2) {
+    const int per = (BLN_NT / 32) * QW2;
+    bln_np_fast<QW2, CAP2><<<(n2 + per - 1) / per, BLN_NT, sm2, st>>>(h->d_rowptr, h->d_colidx, xy, n, qp,
+                                                                     sp + n1, n2, jac.as<double>());
+    ++launches;
+  }
+  if (n3) {
+    blm_np_kernel<<<2 * h->num_sms, 512, 0, st>>>(h->d_rowptr, h->d_colidx, xy, n, qp, sp + n1 + n2, n3,
+                                                  jac.as<double>());
+    ++launches;
+  }
   blm_np_reduce<<<1, BLM_RT, 0, st>>>(jac.as<double>(), nq, out.as<double>(), cnt.as<int>());
   BL_CUDA(h, cudaGetLastError());
   BL_CUDA(h, mark(h, 1, st));
@@ -191,6 +249,6 @@ extern "C" bl_status bl_neighborhood_preservation(bl_ctx *h, const float *d_xy,
   BL_CUDA(h, cudaStreamSynchronize(st));
   if (counted) *counted = c;
   record_time(h);
-  h->launches = 2;
+  h->launches = launches;
   return BL_OK;
 }

@@ -74,3 +74,45 @@ def test_layout_improves_quality():
     st0 = oracle.stress(g.n, g.rowptr, g.colidx, xr)[0]
     st1 = _metrics(g, out)[1][0]
     assert st1 <= 0.5 * st0, (st1, st0)
+
+
+def _mixed_degree_graph(n, seed):
+    """A hub joined to every other vertex, a band of vertices of degree ~40-120
+    and a sparse remainder: the queries of all three NP kernels (kk <= 32,
+    kk <= 256, radix select) in one graph."""
+    rng = np.random.default_rng(seed)
+    src, dst = [np.zeros(n - 1, np.int64)], [np.arange(1, n)]
+    for v in range(1, 40):
+        nb = rng.choice(np.arange(1, n), rng.integers(40, 120), replace=False)
+        src.append(np.full(nb.size, v))
+        dst.append(nb)
+    src.append(rng.integers(1, n, 3 * n))
+    dst.append(rng.integers(1, n, 3 * n))
+    s, d = np.concatenate(src), np.concatenate(dst)
+    keep = s != d
+    return edges_to_csr(n, s[keep], d[keep])
+
+
+@pytest.mark.parametrize("lattice", [None, 4, 16])
+def test_np_three_paths_with_ties(lattice):
+    """NP routed through the one-scan threshold kernels and the radix select
+    (kk <= 32 / <= 256 / above), on continuous positions and on coarse integer
+    lattices where most squared distances tie (ties by vertex id, M3): the
+    counted queries and the NP value agree with the oracle exactly."""
+    import paper_2002_08233_b200 as bl
+    n = 1500
+    g = _mixed_degree_graph(n, 5)
+    deg = np.diff(g.rowptr)
+    assert deg.max() > 256 and ((deg > 32) & (deg <= 256)).any() and (deg <= 32).any()
+    xy = uniform_coords(n, 9)
+    if lattice is not None:
+        xy = np.floor(xy * lattice).astype(np.float32)
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = _dev(xy)
+        got = bl.bl_neighborhood_preservation(lay.h, d, None)
+        q = np.arange(n - 1, -1, -3, dtype=np.int32)        # an unordered subset
+        got_q = bl.bl_neighborhood_preservation(lay.h, d, q)
+    ref = oracle.neighborhood_preservation(g.n, g.rowptr, g.colidx, xy)
+    ref_q = oracle.neighborhood_preservation(g.n, g.rowptr, g.colidx, xy, q)
+    assert got[1] == ref[1] and got[0] == pytest.approx(ref[0], rel=1e-14, abs=1e-15)
+    assert got_q[1] == ref_q[1] and got_q[0] == pytest.approx(ref_q[0], rel=1e-14, abs=1e-15)
