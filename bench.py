@@ -579,15 +579,27 @@ def bench_attraction(lay, d_xy0, params, stream, flush, g, peaks):
     p = dict(params, flags=int(params.get("flags", 0)) | bl.BL_ATTRACTION_ONLY)
     nbytes = 12 * g.nnz + 4 * (g.n + 1) + 16 * g.n
     out = {}
-    for mode in ("l2_warm", "hbm_cold"):
+    # l2_warm: the average launch duration over 20 back-to-back launches
+    # (CUDA events around all of them on the launching stream)
+    lay.forces(d_xy0, 0, g.n, stream=stream, **p)
+    torch.cuda.synchronize()
+    reps = 20
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        lay.forces(d_xy0, 0, g.n, stream=stream, **p)
+    b.record(stream)
+    b.synchronize()
+    t = a.elapsed_time(b) / reps / 1e3
+    out["l2_warm"] = {"us": 1e6 * t, "GB_per_s": nbytes / t / 1e9, "launches_timed": reps,
+                      "frac_of_hbm_peak": nbytes / t / 1e9 / float(peaks.get("hbm_gbs", 6540.2))}
+    # hbm_cold: L2 flushed before each launch, the median of 5 single launches
+    for mode in ("hbm_cold",):
         lay.forces(d_xy0, 0, g.n, stream=stream, **p)
         torch.cuda.synchronize()
         ms = []
         for i in range(5):
-            if mode == "hbm_cold":
-                flush.fill_(float(i))
-            else:  # keep the GPU busy while the host enqueues (kernel time, not call latency)
-                torch.cuda._sleep(100000)
+            flush.fill_(float(i))
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             lay.forces(d_xy0, 0, g.n, stream=stream, **p)
