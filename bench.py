@@ -486,23 +486,28 @@ def _time_layout(lay, d_xy0, params, stream, flush, steps, warmup=2):
 
 def bench_shuffle(args, lay, d_xy0, params, stream, flush, cfg, t_default):
     """Secondary object: batch randomisation (shuffle_seed, §4.3.3)
-    on the same workload -- it runs on the two-barrier driver, so the cost is
-    split into the driver (sequential batches on the two-barrier driver) and
-    the reshuffle itself ("Randomization also introduces overhead")."""
+    on the same workload ("Randomization also introduces overhead").
+    Default: every iteration relabelled into position space (one extra launch,
+    csrc/bl_relabel.cu) and run by the sequential driver; `inkernel` is the
+    round-2 first version, randomised inside the two-barrier driver
+    (BL_SHUFFLE_RELABEL=0; still used with tol > 0)."""
     import paper_2002_08233_b200 as bl
     steps = max(2, min(args.steps, 3))
     t_shuf = _time_layout(lay, d_xy0, dict(params, shuffle_seed=1), stream, flush, steps)
     drv = bl.bl_driver_name(lay.h)
-    os.environ["BL_PIPELINE"] = "0"
+    launches = bl.bl_last_launch_count(lay.h)
+    os.environ["BL_SHUFFLE_RELABEL"] = "0"
     try:
-        t_seq2 = _time_layout(lay, d_xy0, params, stream, flush, steps)
+        t_ik = _time_layout(lay, d_xy0, dict(params, shuffle_seed=1), stream, flush, 2, warmup=1)
+        drv_ik = bl.bl_driver_name(lay.h)
     finally:
-        os.environ.pop("BL_PIPELINE", None)
+        os.environ.pop("BL_SHUFFLE_RELABEL", None)
     return {"shuffle_seed": 1, "driver": drv, "iters_per_sec": cfg.iters / t_shuf,
-            "ms_per_step": 1e3 * t_shuf,
-            "sequential_same_driver_iters_per_sec": cfg.iters / t_seq2,
+            "ms_per_step": 1e3 * t_shuf, "gpu_launches_per_step": launches,
             "default_iters_per_sec": cfg.iters / t_default,
-            "cost_vs_default": t_shuf / t_default, "cost_of_reshuffle_alone": t_shuf / t_seq2}
+            "cost_vs_default": t_shuf / t_default,
+            "inkernel": {"driver": drv_ik, "iters_per_sec": cfg.iters / t_ik,
+                         "cost_vs_default": t_ik / t_default}}
 
 
 def bench_metrics(lay, d_xy, g, peaks, sm_mhz, nsm, stream, sources=1024):

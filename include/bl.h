@@ -91,8 +91,12 @@ typedef struct {
                           walks the batches of a fresh seeded permutation
                           pi_it of the vertex ids (batch t = pi_it(t b ..)),
                           a keyed Feistel bijection any implementation can
-                          evaluate.  BL_ALGO_EXACT only (BL_EINVAL with BH);
-                          runs on the two-barrier driver     */
+                          evaluate.  BL_ALGO_EXACT only (BL_EINVAL with BH).
+                          Each iteration is relabelled into position space
+                          (one extra launch) and runs on the sequential
+                          drivers; with tol > 0, or where those do not apply,
+                          the two-barrier driver randomises in the kernel
+                                                              */
 } bl_params;
 
 /* Fill p with the paper's defaults: iters 600 (the CLI default),
@@ -172,9 +176,14 @@ bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits);
  * undirected edge once; 0 for a graph without edges. */
 bl_status bl_edge_uniformity(bl_ctx *h, const float *d_xy, double *eu, void *cuda_stream);
 
-/* Scale-optimised stress: sum over ordered pairs (i, j), i in the
+/* Scale-optimised stress: sum over ORDERED pairs (i, j), i in the
  * source set, j != i reachable, of (s ||c_i - c_j|| - d_ij)^2 / d_ij^2 with
- * d_ij = BFS hop distance and s = s* minimising it (closed form).  sources:
+ * d_ij = BFS hop distance and s = s* minimising it (closed form).  With all
+ * n sources every unordered pair {i, j} is therefore counted twice: stress,
+ * pairs and unreachable are 2x the unordered-pair (i < j) values SPEC.md's
+ * program reports; s* is the same (reading M1 of DESIGN.md §3: a source
+ * subset has no i < j form, so the ordered sum is the one definition that
+ * covers both).  sources:
  * host int32[nsrc] (NULL = all n vertices, nsrc ignored); scale (nullable) <-
  * s*; pairs (nullable) <- reachable pairs; unreachable (nullable) <- pairs
  * excluded because j is not reachable from i.  BL_EINVAL on a bad source. */

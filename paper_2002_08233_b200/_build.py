@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbl.so")
 # one translation unit per kernel group: nvcc runs them in parallel
 SOURCES = ["bl_exact_v0.cu", "bl_bh.cu", "bl_exact_v1.cu", "bl_exact_v2.cu", "bl_exact_v3.cu",
-           "bl_exact_v4.cu", "bl_cluster.cu", "bl_metrics.cu", "bl_attr.cu", "bl_api.cu", "bl_microbench.cu",
+           "bl_exact_v4.cu", "bl_cluster.cu", "bl_metrics.cu", "bl_attr.cu", "bl_relabel.cu", "bl_api.cu", "bl_microbench.cu",
            "bl_init.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

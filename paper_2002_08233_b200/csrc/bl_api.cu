@@ -352,6 +352,7 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_la_lpart);
   cudaFree(h->d_la_cls);
   cudaFree(h->d_la_bar);
+  bl_relabel_free(h);
   cudaFree(h->d_chk);
   cudaFree(h->d_part_st);
   cudaFree(h->d_pend_st);
@@ -407,8 +408,21 @@ static int max_items_per_batch(const bl_ctx *h, int b, int first, int count) {
 
 // Launch the persistent kernel.  forces_mode: one "batch" [first, first+count)
 // whose forces are written to f_out instead of being applied.
+// rl (batch randomisation by relabelling, bl_relabel.cu): one iteration in
+// position space -- the CSR, energy slot and iteration counter it names
+// replace the context's, shuffle_seed is ignored (the batches are contiguous
+// there); rl->probe only reports which driver the launch would take.
+struct BLRelabelRun {
+  const int *rowptr, *colidx;
+  double *energy;
+  int *iters_done;
+  int probe;      // in: 1 = no launch, out: pipelined
+  int pipelined;  // out: BLKParams::pipelined of this (n, b)
+  int it;         // iteration (checked builds: the violation record is zeroed at it = 0 only)
+};
 static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
-                        int forces_mode, int first, int count, float2 *f_out) {
+                        int forces_mode, int first, int count, float2 *f_out,
+                        BLRelabelRun *rl = nullptr) {
   const int n = h->n;
   const int b = forces_mode ? std::max(1, count) : std::min(p->batch, n);
   const int G = h->G;
@@ -447,8 +461,8 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.first = first;
   k.count = count;
   k.xy = d_xy;
-  k.rowptr = h->d_rowptr;
-  k.colidx = h->d_colidx;
+  k.rowptr = rl ? rl->rowptr : h->d_rowptr;
+  k.colidx = rl ? rl->colidx : h->d_colidx;
   k.item_ptr = h->d_item_ptr;
   k.item_v = h->d_item_v;
   k.item_k0 = h->d_item_k0;
@@ -476,7 +490,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
                                               : find_variant(h->NT, h->T, h->TP);
   // batch randomisation (readings R1-R2): the two-barrier driver (its phase U
   // takes batch positions, not owned vertices)
-  k.shuf_seed = forces_mode ? 0ull : (unsigned long long)p->shuffle_seed;
+  k.shuf_seed = (forces_mode || rl) ? 0ull : (unsigned long long)p->shuffle_seed;
   k.shuf_h = 1;
   while ((1LL << (2 * k.shuf_h)) < (long long)n) ++k.shuf_h;
   k.pipelined = !forces_mode && k.shuf_seed == 0 && k.nb >= 4 && b <= BL_TGT_CAP && (b % 2) == 0 &&
@@ -486,11 +500,16 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.part_nbuf = 2;
   k.attr = h->d_attr;
   k.e_cta = h->d_e_cta;
-  k.energy = h->d_energy;
-  k.iters_done = h->d_iters_done;
+  k.energy = rl ? rl->energy : h->d_energy;
+  k.iters_done = rl ? rl->iters_done : h->d_iters_done;
   k.bar = h->d_bar;
   k.f_out = f_out;
   k.prof = h->d_prof;
+  if (rl) {
+    rl->pipelined = k.pipelined;
+    // the two-barrier driver's phase U walks the vertex-space items
+    if (rl->probe || !k.pipelined) return BL_OK;
+  }
 
   if (attr_only) {
     // step a5 alone: the standalone high-occupancy kernels (bl_attr.cuh)
@@ -566,7 +585,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   }
   if ((s = grow(h, h->d_part_st, h->part_st_cap, (size_t)3 * b * G)) != BL_OK) return s;
   if ((s = grow(h, h->d_pend_st, h->pend_st_cap, (size_t)2 * b)) != BL_OK) return s;
-  BL_CUDA(h, cudaMemsetAsync(h->d_chk, 0, sizeof(unsigned) * 8, st));
+  if (!rl || rl->it == 0) BL_CUDA(h, cudaMemsetAsync(h->d_chk, 0, sizeof(unsigned) * 8, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_xy_st, 0, sizeof(unsigned) * (size_t)n, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_part_st, 0, sizeof(unsigned) * h->part_st_cap, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_pend_st, 0, sizeof(unsigned) * h->pend_st_cap, st));
@@ -577,6 +596,11 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.jitter = (unsigned)env_int("BL_JITTER", 0);
   k.chk_break = env_int("BL_CHK_BREAK", 0);
 #endif
+  // long CSR rows in update tasks: 8 gathers in flight per lane on the async
+  // driver (measured +1.4 % at C5, -1..2 % on the latency-bound configs with
+  // sequential batches, whose hubs sit in the first batches); with relabelled
+  // randomised batches every batch holds hub rows (BL_LONG8 overrides)
+  k.long8 = env_int("BL_LONG8", (k.pipelined == 2 || rl) ? 1 : 0);
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   h->driver_last = forces_mode ? "two-barrier"
@@ -594,7 +618,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   BL_CUDA(h, cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned), st));
   // forces mode never writes iters_done: leave the last layout call's count
   // (and its energy trace) to bl_energy
-  if (!forces_mode) BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+  if (!forces_mode) BL_CUDA(h, cudaMemsetAsync(k.iters_done, 0, sizeof(int), st));
   if (h->d_prof) BL_CUDA(h, cudaMemsetAsync(h->d_prof, 0, sizeof(unsigned long long) * (16 + G), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(vt->NT), args, smem, st));
@@ -719,16 +743,21 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
 
 // Small graphs: the exact method on one thread-block cluster (bl_cluster.cuh)
 // when a batch's work is small enough that the whole-GPU kernel's per-batch
-// grid barrier dominates (b n <= BL_CLUSTER_PAIRS, default 1e6: measured
-// crossover ~1.5e6 pairs per batch on B200) and the
+// grid barrier dominates (b n <= BL_CLUSTER_PAIRS, default 6e5: the measured
+// crossover against the latency driver on B200) and the
 // coordinates fit every CTA's shared memory.  Returns BL_OK and sets *used.
+// rl: one relabelled iteration (see launch).
 static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
-                                bool *used) {
+                                bool *used, BLRelabelRun *rl = nullptr) {
   *used = false;
   const int n = h->n, b = std::min(p->batch, n);
   if (env_int("BL_CLUSTER", 1) == 0) return BL_OK;
-  if (p->shuffle_seed) return BL_OK;  // randomised batches: whole-GPU two-barrier driver
-  const long long pairs_max = env_int("BL_CLUSTER_PAIRS", 1000000);
+  if (p->shuffle_seed) return BL_OK;  // randomised batches: relabelled, else the two-barrier driver
+  // crossover against the latency driver, re-measured in round 2 on grids
+  // (scripts/cluster_vs_lat.py, us per batch cluster / latency): b n = 262k
+  // 3.2 / 4.2, 352k 3.5 / 3.7, 512k 3.9 / 4.0, 704k 4.3 / 3.8, 1.05M 5.0-6.6 /
+  // 3.8-4.2 (round 1, against the pipelined driver: 1e6)
+  const long long pairs_max = env_int("BL_CLUSTER_PAIRS", 600000);
   if ((long long)b * n > pairs_max) return BL_OK;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
@@ -773,6 +802,10 @@ static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
       continue;
     }
     CS = cs;
+    if (rl && rl->probe) {
+      *used = true;
+      return BL_OK;
+    }
     bl_status s;
     if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
     BLCParams k{};
@@ -795,11 +828,11 @@ static bl_status launch_cluster(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
     k.nnz = h->nnz;
     k.csr_smem = csr_smem ? 1 : 0;
     k.xy = d_xy;
-    k.rowptr = h->d_rowptr;
-    k.colidx = h->d_colidx;
-    k.energy = h->d_energy;
-    k.iters_done = h->d_iters_done;
-    BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
+    k.rowptr = rl ? rl->rowptr : h->d_rowptr;
+    k.colidx = rl ? rl->colidx : h->d_colidx;
+    k.energy = rl ? rl->energy : h->d_energy;
+    k.iters_done = rl ? rl->iters_done : h->d_iters_done;
+    BL_CUDA(h, cudaMemsetAsync(k.iters_done, 0, sizeof(int), st));
     void *args[] = {&k};
     BL_CUDA(h, cudaLaunchKernelExC(&cfg, kfn, args));
     h->launches = 1;
@@ -825,6 +858,70 @@ extern "C" bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits) {
   return BL_OK;
 }
 
+// Batch randomisation by relabelling (bl_relabel.cu): every
+// iteration is one relabel launch + one plain launch of the layout kernel in
+// position space, with whatever sequential driver (asynchronous, latency,
+// pipelined) the size takes.  Taken when the whole-GPU kernel would run one of
+// those drivers and the call has no convergence rule (tol > 0 is decided on
+// the device between iterations: the in-kernel randomisation of the
+// two-barrier driver keeps it); BL_SHUFFLE_RELABEL=0 turns it off.
+// max_batches: the iteration that exhausts the budget gets the rest of it.  The Step of iteration it is
+// step0 cooling^it by the same repeated fp64 product as in the kernel.
+static bl_status layout_relabel(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
+                                bool *used) {
+  *used = false;
+  if (!p->shuffle_seed || p->algo != BL_ALGO_EXACT || p->tol != 0.0 ||
+      env_int("BL_SHUFFLE_RELABEL", 1) == 0)
+    return BL_OK;
+  bl_status s = bl_relabel_alloc(h);
+  if (s != BL_OK) return s;
+  bl_params q = *p;
+  q.iters = 1;
+  q.shuffle_seed = 0;
+  q.max_batches = 0;
+  BLRelabelRun rl{h->d_rowptrP, h->d_colidxP, nullptr, h->d_rl_iters, 1, 0, 0};
+  bool cluster = false;
+  if ((s = launch_cluster(h, h->d_xyP, &q, st, &cluster, &rl)) != BL_OK) return s;
+  if (!cluster) {
+    if ((s = launch(h, h->d_xyP, &q, st, 0, 0, 0, nullptr, &rl)) != BL_OK) return s;
+    if (!rl.pipelined) return BL_OK;
+  }
+  if ((s = grow(h, h->d_energy, h->energy_cap, (size_t)std::max(1, p->iters))) != BL_OK) return s;
+  int shuf_h = 1;
+  while ((1LL << (2 * shuf_h)) < (long long)h->n) ++shuf_h;
+  rl.probe = 0;
+  double step = p->step0;
+  int launches = 0, done = 0;
+  const int b = std::min(p->batch, h->n);
+  const long long nb = (h->n + b - 1) / b;
+  for (int it = 0; it < p->iters; ++it) {
+    const long long left = p->max_batches > 0 ? p->max_batches - it * nb : nb + 1;
+    if ((s = bl_relabel_launch(h, d_xy, (unsigned long long)p->shuffle_seed, shuf_h, it, it > 0,
+                               st)) != BL_OK)
+      return s;
+    q.step0 = step;
+    q.max_batches = left <= nb ? (int)left : 0;  // the budget ends inside this iteration
+    rl.energy = h->d_energy + it;
+    rl.it = it;
+    s = cluster ? launch_cluster(h, h->d_xyP, &q, st, &cluster, &rl)
+                : launch(h, h->d_xyP, &q, st, 0, 0, 0, nullptr, &rl);
+    if (s != BL_OK) return s;
+    launches += 2;
+    if (left <= nb) break;  // iters_done counts completed iterations (as every driver)
+    done = it + 1;
+    step = step * p->cooling;
+  }
+  if ((s = bl_unrelabel_launch(h, d_xy, done, st)) != BL_OK) return s;
+  h->launches = launches + 1;
+  const std::string d = h->driver_last;
+  h->driver_last = d == "async"     ? "relabel+async"
+                   : d == "latency" ? "relabel+latency"
+                   : d == "cluster" ? "relabel+cluster"
+                                    : "relabel+pipelined";
+  *used = true;
+  return BL_OK;
+}
+
 extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p, void *cuda_stream) {
   if (!h) return bl_fail(nullptr, BL_EINVAL, "handle is NULL");
   h->launches = 0;
@@ -845,7 +942,11 @@ extern "C" bl_status bl_layout_device(bl_ctx *h, float *d_xy, const bl_params *p
   snprintf(h->kname_last, sizeof h->kname_last, "%s", p->algo == BL_ALGO_BH ? "bl_bh_kernel<512>" : h->kname);
   h->driver_last = p->algo == BL_ALGO_BH ? "bh" : "";
   bool clustered = false;
-  if (p->algo == BL_ALGO_EXACT) {
+  if (p->algo == BL_ALGO_EXACT && p->shuffle_seed) {
+    s = layout_relabel(h, reinterpret_cast<float2 *>(d_xy), p, st, &clustered);
+    if (s != BL_OK) return s;
+  }
+  if (p->algo == BL_ALGO_EXACT && !clustered) {
     s = launch_cluster(h, reinterpret_cast<float2 *>(d_xy), p, st, &clustered);
     if (s != BL_OK) return s;
   }

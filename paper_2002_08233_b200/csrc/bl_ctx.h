@@ -78,6 +78,12 @@ struct bl_ctx {
   // checked builds (-DBL_CHECKED): violation record and phase stamps
   unsigned *d_chk = nullptr, *d_part_st = nullptr, *d_pend_st = nullptr, *d_xy_st = nullptr;
   size_t part_st_cap = 0, pend_st_cap = 0;
+  // batch randomisation by relabelling (bl_relabel.cu): pi_it, its inverse and
+  // the position-space CSR / coordinates of the current iteration
+  int *d_piv = nullptr, *d_inv = nullptr, *d_rowptrP = nullptr, *d_colidxP = nullptr;
+  int *d_rl_sum = nullptr, *d_rl_iters = nullptr;
+  unsigned *d_rl_bar = nullptr;
+  float2 *d_xyP = nullptr;
   // quality-metric scratch: grown on first use, kept for the context's life
   // (no allocation inside a metric call after the first)
   void *m_scr[24] = {nullptr};
@@ -117,3 +123,10 @@ bl_status bl_long_rows(bl_ctx *h);  // degree classes of the rows (bl_attr.cu), 
 bl_status bl_eu_launch(bl_ctx *h, const float2 *xy, int blocks, double *part, double *stats,
                        cudaStream_t st);
 int bl_eu_blocks(const bl_ctx *h);  // grid of the edge-uniformity kernel
+// bl_relabel.cu: position space of one randomised iteration (one cooperative
+// launch), and the final scatter back to vertex space
+bl_status bl_relabel_alloc(bl_ctx *h);
+void bl_relabel_free(bl_ctx *h);
+bl_status bl_relabel_launch(bl_ctx *h, float2 *xy, unsigned long long seed, int shuf_h, int it,
+                            int unperm, cudaStream_t st);
+bl_status bl_unrelabel_launch(bl_ctx *h, float2 *xy, int iters, cudaStream_t st);

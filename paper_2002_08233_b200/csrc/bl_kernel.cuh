@@ -116,7 +116,8 @@ struct BLKParams {
   float a_half, r_half;  // (a-1)/2, (r-1)/2: vector coefficients d^(a-1), d^(r-1)
   int forces_mode, first, count;
   // batch randomisation (readings R1-R2): 0 = sequential; else
-  // iteration it walks the batches of pi_it (two-barrier driver only)
+  // iteration it walks the batches of pi_it inside the two-barrier driver
+  // (relabelled iterations, bl_relabel.cu, launch with shuf_seed = 0)
   unsigned long long shuf_seed;
   int shuf_h;            // Feistel half width: 2^(2h) >= n
   int attr_only;         // forces_mode + BL_ATTRACTION_ONLY: a5 alone (no sweep, R = 0)
@@ -129,6 +130,9 @@ struct BLKParams {
                          // without CTA-wide barriers between phases (bl_run_async)
   int part_nbuf;         // part buffers (2: pipelined, 3: async)
   int afence_gpu;        // async: GPU-scope fences in every task (debug, BL_AFENCE=1)
+  int long8;             // update tasks walk long CSR rows 256 entries per round (8 gathers
+                         // in flight per lane): the async driver always; the others when
+                         // every batch holds hub rows (relabelled randomised batches)
   float2 *attr;          // [max items per batch]
   double *e_cta;         // [2][G]
   double *energy;        // [iters]
@@ -1115,7 +1119,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     // Measured: +1.4 % at C5 (async driver: shorter updates, less waiting on
     // other CTAs), -1..2 % on the latency-bound configs, which keep the
     // unrolled loop below.
-    if (p.pipelined != 2) {
+    if (!p.long8) {
 #pragma unroll 4
       for (int k = k0 + lane; k < k1; k += 32) {
         const int j = __ldg(p.colidx + k);

@@ -641,10 +641,12 @@ def test_fuzz_shapes_async_forced(case, env, monkeypatch):
 
 @pytest.mark.parametrize("name,expect", [("C2", "latency"), ("C3b256", "latency"),
                                          ("C3b1024", "latency"), ("C4", "latency"),
-                                         ("C1", "cluster"), ("C3b64", "cluster")])
+                                         ("C1", "cluster"), ("C3b64", "latency"),
+                                         ("C5", "async")])
 def test_default_driver_per_config(name, expect):
-    """The measured crossovers: single cluster for b n <= 1e6, the latency
-    driver up to b n = 2^24, asynchronous phases above."""
+    """The measured crossovers: single cluster for b n <= 6e5 (C3 b=64, 7.0e5,
+    went to the latency driver in round 2: 4.3 -> 3.8 us per batch), the
+    latency driver up to b n = 2^24, asynchronous phases above."""
     import torch
 
     import paper_2002_08233_b200 as bl

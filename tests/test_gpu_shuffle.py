@@ -2,7 +2,12 @@
 R1-R2 of DESIGN.md §3) vs the oracle's, through the C-ABI.  Marked gpu.
 
 Both sides evaluate the same keyed Feistel permutation pi_it with integer
-arithmetic (no shared code: oracle/bl_oracle.c vs csrc/bl_kernel.cuh)."""
+arithmetic (no shared code: oracle/bl_oracle.c vs csrc/bl_kernel.cuh).
+
+Two GPU realisations: by default every iteration is relabelled
+into position space (csrc/bl_relabel.cu) and runs on the sequential drivers;
+BL_SHUFFLE_RELABEL=0 (or tol > 0) randomises inside the two-barrier driver.
+`mode` runs both."""
 import numpy as np
 import pytest
 
@@ -15,6 +20,19 @@ pytestmark = pytest.mark.gpu
 
 ALL = ["C1", "C2", "C3b64", "C3b256", "C3b1024", "C4", "C5"]
 SEED = 20022
+
+
+MODES = ["relabel", "inkernel"]
+
+
+@pytest.fixture
+def mode(request, monkeypatch):
+    m = getattr(request, "param", "relabel")
+    if m == "inkernel":
+        monkeypatch.setenv("BL_SHUFFLE_RELABEL", "0")
+    else:
+        monkeypatch.delenv("BL_SHUFFLE_RELABEL", raising=False)
+    return m
 
 
 def _params(cfg, **kw):
@@ -31,8 +49,9 @@ def _oracle(g, xy0, p):
                          shuffle_seed=p["shuffle_seed"])
 
 
+@pytest.mark.parametrize("mode", MODES, indirect=True)
 @pytest.mark.parametrize("name", ALL)
-def test_shuffled_one_batch_parity(name):
+def test_shuffled_one_batch_parity(name, mode):
     """One randomised batch (pi_0(0 .. b-1)): positions vs the oracle, and
     exactly the batch's members may move."""
     g, xy0, cfg = build_config(name)
@@ -45,8 +64,9 @@ def test_shuffled_one_batch_parity(name):
     assert np.array_equal(got[others], xy0[others])
 
 
+@pytest.mark.parametrize("mode", MODES, indirect=True)
 @pytest.mark.parametrize("name", ALL)
-def test_shuffled_one_iteration_parity(name):
+def test_shuffled_one_iteration_parity(name, mode):
     g, xy0, cfg = build_config(name)
     p = _params(cfg, iters=1)
     got, tr, done = gpu_layout(g, xy0, **p)
@@ -57,7 +77,8 @@ def test_shuffled_one_iteration_parity(name):
                         what=f"{name} shuffled one iteration")
 
 
-def test_shuffled_iterations_use_fresh_permutations():
+@pytest.mark.parametrize("mode", MODES, indirect=True)
+def test_shuffled_iterations_use_fresh_permutations(mode):
     """Iteration 1 walks pi_1, not pi_0: shadowed second iteration (from the
     GPU's state after one iteration, the oracle's second iteration with the
     cooled step) -- via max_batches inside iteration 1."""
@@ -94,8 +115,9 @@ def test_shuffled_b_equals_n_matches_sequential():
     assert_energy_close(eb[:1], ea[:1], tol=2e-6, what="b = n shuffled vs sequential")
 
 
+@pytest.mark.parametrize("mode", MODES, indirect=True)
 @pytest.mark.parametrize("name", ["C1", "C4"])
-def test_shuffled_determinism_bitwise(name):
+def test_shuffled_determinism_bitwise(name, mode):
     g, xy0, cfg = build_config(name)
     p = _params(cfg, iters=3)
     a, ea, _ = gpu_layout(g, xy0, **p)
@@ -103,13 +125,96 @@ def test_shuffled_determinism_bitwise(name):
     assert np.array_equal(a, b) and np.array_equal(ea, eb)
 
 
-def test_shuffled_driver_and_rejections():
+@pytest.mark.parametrize("mode", MODES, indirect=True)
+def test_shuffled_later_iterations_shadowed(mode):
+    """Iterations 1 and 2 (pi_1, pi_2, the cooled Steps, the energy slots),
+    each shadowed from the GPU's own state before it: the oracle cannot start
+    at iteration k, but a randomised iteration is the sequential iteration of
+    the graph relabelled by pi_k (pinned for the oracle in
+    tests/test_oracle_shuffle_pins.py), so the reference is the oracle's
+    sequential path on that graph with Step = step0 cooling^k.  (Free-running
+    traces separate by rounding after the first iteration -- every vertex
+    moves a full Step along its force direction -- which is why later
+    iterations are shadowed.)"""
+    from tests.test_oracle_shuffle_pins import relabelled
+    g, xy0, cfg = build_config("C3b256")
+    states, traces = [xy0], []
+    for k in (1, 2, 3):
+        xy, tr, done = gpu_layout(g, xy0, **_params(cfg, iters=k))
+        assert done == k
+        states.append(xy)
+        traces.append(tr)
+    assert np.array_equal(traces[2][:2], traces[1][:2]) and np.array_equal(traces[1][:1], traces[0])
+    for k in (1, 2):
+        perm = oracle.permutation(g.n, SEED, k)
+        gp, xyp = relabelled(g, states[k], perm)
+        q = dict(iters=1, batch=cfg.batch, K=cfg.K, C=cfg.C, step0=cfg.step0 * cfg.cooling ** k,
+                 cooling=cfg.cooling)
+        refp, Ep, _ = oracle.layout(gp.n, gp.rowptr, gp.colidx, xyp, **q)
+        ref = np.empty_like(refp)
+        ref[perm] = refp
+        # the energy (a sum over all vertices) and the bulk of the positions to
+        # the one-iteration gates.  Not the maximum: in the contracted layout
+        # of a later iteration a few vertices' forces nearly cancel (|f| <<
+        # sum |terms|), and since every vertex moves a full Step ALONG f, the
+        # fp32 direction error u32 sum|terms| / |f| (DESIGN.md §6) reaches
+        # 1e-3..1e-2 x extent for a handful of them (measured, both
+        # realisations: median 1e-8, p99 5e-7..4e-5, max 1e-4..1.7e-2) -- a
+        # wrong permutation, Step or batch order moves EVERY vertex by O(Step)
+        ext = float(np.ptp(ref, axis=0).max())
+        err = np.abs(states[k + 1] - ref).max(axis=1) / ext
+        print(f"{mode} iteration {k}: median {np.median(err):.2e} p99 {np.quantile(err, 0.99):.2e} "
+              f"max {err.max():.2e} E rel {abs(traces[2][k] - Ep[0]) / Ep[0]:.2e}")
+        assert np.median(err) <= 1e-6, float(np.median(err))
+        assert np.quantile(err, 0.99) <= POS_TOL, float(np.quantile(err, 0.99))
+        assert np.mean(err > POS_TOL) <= 0.005, float(np.mean(err > POS_TOL))
+        assert_energy_close(traces[2][k:k + 1], Ep[:1], tol=max(1e-5, energy_gate(gp, xyp, q)),
+                            what=f"shuffled iteration {k} shadowed")
+
+
+@pytest.mark.parametrize("mb", [1, 43, 44, 86, 87, 1000])
+def test_relabelled_max_batches_and_iters_done(mb):
+    """The batch budget across relabelled iterations (nb = 43 at C3 b=256):
+    iters_done counts completed iterations exactly as the oracle does (a
+    budget that ends with an iteration's last batch does not complete it),
+    and exactly the batches within the budget have moved."""
+    g, xy0, cfg = build_config("C3b256")
+    nb = -(-g.n // cfg.batch)
+    assert nb == 43
+    p = _params(cfg, iters=3, max_batches=mb)
+    a, _, da = gpu_layout(g, xy0, **p)
+    _, _, dr = _oracle(g, xy0, p)
+    assert da == dr
+    # vertices of batches beyond the budget have not moved
+    moved = np.zeros(g.n, bool)
+    left = mb
+    for it in range(3):
+        k = min(left, nb)
+        moved[oracle.permutation(g.n, SEED, it)[:min(k * cfg.batch, g.n)]] = True
+        left -= k
+        if left <= 0:
+            break
+    assert np.array_equal(a[~moved], xy0[~moved])
+    assert (a[moved] != xy0[moved]).any(axis=1).all()
+
+
+def test_shuffled_driver_and_rejections(monkeypatch):
     import torch
 
     import paper_2002_08233_b200 as bl
     g, xy0, cfg = build_config("C5")
     with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
         d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, iters=1, batch=1024, max_batches=2, shuffle_seed=SEED)
+        torch.cuda.synchronize()
+        assert bl.bl_driver_name(lay.h) == "relabel+async"
+        assert bl.bl_last_launch_count(lay.h) == 3  # relabel, layout, scatter back
+        # a convergence rule keeps the in-kernel randomisation
+        lay.layout_device(d, iters=1, batch=1024, max_batches=2, shuffle_seed=SEED, tol=1e-30)
+        torch.cuda.synchronize()
+        assert bl.bl_driver_name(lay.h) == "two-barrier"
+        assert bl.bl_last_launch_count(lay.h) == 1
+        monkeypatch.setenv("BL_SHUFFLE_RELABEL", "0")
         lay.layout_device(d, iters=1, batch=1024, max_batches=2, shuffle_seed=SEED)
         torch.cuda.synchronize()
         assert bl.bl_driver_name(lay.h) == "two-barrier"

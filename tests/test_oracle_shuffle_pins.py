@@ -169,3 +169,36 @@ def test_shuffled_thread_count_invariance_bitwise():
     b, Eb, _ = oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=2, batch=64, threads=4,
                              shuffle_seed=3)
     assert np.array_equal(a, b) and np.array_equal(Ea, Eb)
+
+
+def relabelled(g, xy, perm):
+    """The graph and state in POSITION space of `perm` (position i holds
+    vertex perm[i]): numpy only -- the identity behind the GPU's relabelled
+    iterations (csrc/bl_relabel.cu), restated here for the oracle."""
+    n = g.n
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    rows = np.repeat(np.arange(n), np.diff(g.rowptr))
+    gp = edges_to_csr(n, inv[rows], inv[np.asarray(g.colidx)])
+    return gp, np.asarray(xy)[perm]
+
+
+@pytest.mark.parametrize("b", [1, 7, 64])
+def test_shuffled_iteration_is_sequential_on_the_relabelled_graph(b):
+    """Reading R1: the batches of pi_it are the CONTIGUOUS batches of the
+    graph relabelled by pi_it, so a randomised iteration equals a sequential
+    iteration (seed 0) of the relabelled problem, scattered back -- up to the
+    order of the fp64 sums over the other vertices (1e-12).  Pins the
+    oracle's batch membership, its per-batch freezing and the energy against
+    its own sequential path on a different graph."""
+    g = rmat_graph(8, 4, 0.57, 0.19, 0.19, 1)
+    xy0 = uniform_coords(g.n, 3)
+    seed = 77
+    got, E, _ = oracle.layout(g.n, g.rowptr, g.colidx, xy0, iters=1, batch=b, shuffle_seed=seed)
+    perm = oracle.permutation(g.n, seed, 0)
+    gp, xyp = relabelled(g, xy0, perm)
+    refp, Ep, _ = oracle.layout(gp.n, gp.rowptr, gp.colidx, xyp, iters=1, batch=b)
+    ref = np.empty_like(refp)
+    ref[perm] = refp
+    assert np.abs(got - ref).max() <= 1e-11 * np.ptp(ref, axis=0).max()
+    assert abs(E[0] - Ep[0]) <= 1e-11 * Ep[0]
