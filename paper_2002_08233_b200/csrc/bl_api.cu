@@ -264,6 +264,21 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
     h->item_ptr[v + 1] = h->item_ptr[v] + (deg + BL_ECH - 1) / BL_ECH;
   }
   h->n_items = h->item_ptr[n];
+  // BatchLayoutBH: the items of split vertices (rows of more than one item)
+  // as one list in vertex order, {item, vertex, k0, k1} each, with split_ptr[v]
+  // = the number of them below vertex v: a batch's edge-parallel pass walks
+  // split_ptr[lo] .. split_ptr[hi] only, and its inputs are prefetchable
+  std::vector<int> split_ptr((size_t)n + 1, 0);
+  std::vector<int4> sitems;
+  for (int32_t v = 0; v < n; ++v) {
+    const int cnt = h->item_ptr[v + 1] - h->item_ptr[v];
+    split_ptr[v + 1] = split_ptr[v] + (cnt > 1 ? cnt : 0);
+    if (cnt > 1)
+      for (int a = h->item_ptr[v]; a < h->item_ptr[v + 1]; ++a) {
+        const int k0 = rowptr[v] + (a - h->item_ptr[v]) * BL_ECH;
+        sitems.push_back(make_int4(a, v, k0, std::min(k0 + BL_ECH, (int)rowptr[v + 1])));
+      }
+  }
   // item_k0 has a sentinel: item_k0[n_items] = nnz, so item a ends at item_k0[a + 1]
   std::vector<int> item_v(std::max(1, h->n_items)), item_k0((size_t)h->n_items + 1, nnz);
   for (int32_t v = 0; v < n; ++v)
@@ -280,6 +295,8 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   ALLOC(h->d_rowptr, sizeof(int) * ((size_t)n + 1));
   ALLOC(h->d_colidx, sizeof(int) * std::max<size_t>(1, nnz));
   ALLOC(h->d_item_ptr, sizeof(int) * ((size_t)n + 1));
+  ALLOC(h->d_split_ptr, sizeof(int) * ((size_t)n + 1));
+  ALLOC(h->d_sitems, sizeof(int4) * std::max<size_t>(1, sitems.size()));
   ALLOC(h->d_item_v, sizeof(int) * item_v.size());
   ALLOC(h->d_item_k0, sizeof(int) * item_k0.size());
   ALLOC(h->d_iters_done, sizeof(int));
@@ -291,6 +308,9 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
   if (cp(h->d_rowptr, rowptr, sizeof(int) * ((size_t)n + 1)) != cudaSuccess ||
       (nnz > 0 && cp(h->d_colidx, colidx, sizeof(int) * (size_t)nnz) != cudaSuccess) ||
       cp(h->d_item_ptr, h->item_ptr.data(), sizeof(int) * ((size_t)n + 1)) != cudaSuccess ||
+      cp(h->d_split_ptr, split_ptr.data(), sizeof(int) * ((size_t)n + 1)) != cudaSuccess ||
+      (!sitems.empty() &&
+       cp(h->d_sitems, sitems.data(), sizeof(int4) * sitems.size()) != cudaSuccess) ||
       cp(h->d_item_v, item_v.data(), sizeof(int) * item_v.size()) != cudaSuccess ||
       cp(h->d_item_k0, item_k0.data(), sizeof(int) * item_k0.size()) != cudaSuccess)
     return bad(bl_fail(h, BL_ECUDA, "CSR upload failed"));
@@ -310,6 +330,8 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_rowptr);
   cudaFree(h->d_colidx);
   cudaFree(h->d_item_ptr);
+  cudaFree(h->d_split_ptr);
+  cudaFree(h->d_sitems);
   cudaFree(h->d_item_v);
   cudaFree(h->d_item_k0);
   cudaFree(h->d_part);
@@ -717,6 +739,9 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.nleaf = h->d_nleaf;
   k.leafv = h->d_leafv;
   k.precompute = !forces_mode && env_int("BL_BH_PRE", 1) != 0;
+  k.pre2 = env_int("BL_BH_PRE2", 1) != 0;
+  k.split_ptr = h->d_split_ptr;
+  k.sitems = h->d_sitems;
   k.e_cta = h->d_e_cta;
   k.energy = h->d_energy;
   k.iters_done = h->d_iters_done;

@@ -37,7 +37,10 @@
 #define BH_FCAP 512  // frontier entries per buffer per warp
 #define BH_TOP_LEVEL 4  // tree levels 0..4 are copied to shared memory per CTA
 #define BH_TOP_MAX 352  // >= 1 + 4 + 16 + 64 + 256
-#define BH_LCAP 32      // leaf vertices recorded per query (one per lane)
+#ifndef BH_LCAP
+#define BH_LCAP 32      // leaf vertices recorded per query (a multiple of 32: BH_LPL per lane)
+#endif
+#define BH_LPL (BH_LCAP / 32)
 
 struct BHKParams {
   int n, b, nb, iters, max_batches;
@@ -79,10 +82,13 @@ struct BHKParams {
   int *nleaf;                  // [n]
   int *leafv;                  // [n][BH_LCAP]
   int precompute;              // 1: use the above
+  int pre2;                    // 1: batch inputs prefetched across the grid barrier (bh_prefetch)
   // attraction of high-degree ("split") vertices, edge-parallel: rows cut in
   // items of <= BL_ECH entries (the context's item lists), one partial per
   // item, published with a release flag stamped with the batch number
   const int *item_ptr, *item_v, *item_k0;
+  const int *split_ptr;        // [n + 1] items of split vertices below v
+  const int4 *sitems;          // those items in vertex order: {item, vertex, k0, k1}
   float2 *attr;                // [n_items]
   unsigned *aflag;             // [n_items]
   unsigned long long *prof;    // optional phase profile (BL_PROFILE=1)
@@ -645,27 +651,30 @@ __device__ __forceinline__ void bh_walk_subtree(const BHKParams &p, int k, int e
 // Attraction sum over CSR entries [k0, k1) of vertex v at cv (one warp,
 // lanes strided, fixed butterfly): f_a = d^2/K along the unit vector
 // (Alg. S3 lines 15-17), live neighbour coordinates.
+// one CSR entry's attraction f_a(d)/d = d^(a-1)/K along Δ = cj - cv
+__device__ __forceinline__ void bh_attr_term(const BHKParams &p, float2 cj, float2 cv, float &fx,
+                                             float &fy) {
+  const float dx = cj.x - cv.x, dy = cj.y - cv.y;
+  const float d2 = fmaf(dx, dx, dy * dy);
+  if (d2 > 0.f) {
+    float at;
+    switch (p.amode) {
+      case 0: at = sqrtf(d2); break;
+      case 1: at = 1.f; break;
+      case 2: at = rsqrtf(d2); break;
+      case 3: at = d2; break;
+      default: at = bl_pow_d2(d2, p.a_half);
+    }
+    fx = fmaf(at * p.invK, dx, fx);
+    fy = fmaf(at * p.invK, dy, fy);
+  }
+}
 __device__ __forceinline__ void bh_attr_lane(const BHKParams &p, int k0, int k1, float2 cv,
                                              int plo, int phi, const float2 *pend, float &fx,
                                              float &fy) {
   const int lane = threadIdx.x & 31;
-  for (int k = k0 + lane; k < k1; k += 32) {
-    const float2 cj = bh_live(p, __ldg(p.colidx + k), plo, phi, pend);
-    const float dx = cj.x - cv.x, dy = cj.y - cv.y;
-    const float d2 = fmaf(dx, dx, dy * dy);
-    if (d2 > 0.f) {
-      float at;  // f_a(d)/d = d^(a-1)/K
-      switch (p.amode) {
-        case 0: at = sqrtf(d2); break;
-        case 1: at = 1.f; break;
-        case 2: at = rsqrtf(d2); break;
-        case 3: at = d2; break;
-        default: at = bl_pow_d2(d2, p.a_half);
-      }
-      fx = fmaf(at * p.invK, dx, fx);
-      fy = fmaf(at * p.invK, dy, fy);
-    }
-  }
+  for (int k = k0 + lane; k < k1; k += 32)
+    bh_attr_term(p, bh_live(p, __ldg(p.colidx + k), plo, phi, pend), cv, fx, fy);
 }
 __device__ __forceinline__ float2 bh_attr_range(const BHKParams &p, int k0, int k1, float2 cv,
                                                 int plo, int phi, const float2 *pend) {
@@ -837,26 +846,32 @@ __device__ __forceinline__ float2 bh_force_pre(const BHKParams &p, int v, float2
                                                int plo, int phi, const float2 *pend,
                                                unsigned stamp) {
   const int lane = threadIdx.x & 31;
-  // first-level loads of both chains together: the leaf id and the row bounds
-  const int j = lane < nl ? __ldcg(p.leafv + (size_t)v * BH_LCAP + lane) : -1;
+  // first-level loads of both chains together: the leaf ids and the row bounds
+  int j[BH_LPL];
+#pragma unroll
+  for (int u = 0; u < BH_LPL; ++u)
+    j[u] = lane + 32 * u < nl ? __ldcg(p.leafv + (size_t)v * BH_LCAP + lane + 32 * u) : -1;
   const int ip0 = __ldg(p.item_ptr + v), ip1 = __ldg(p.item_ptr + v + 1);
   const int k0 = __ldg(p.rowptr + v), k1 = __ldg(p.rowptr + v + 1);
   const float2 cf = __ldcg(p.cellf + v);
   const bool split = ip1 - ip0 > 1;
   // per-lane sums of both chains, one reduction at the end
   float fx = 0.f, fy = 0.f, ax = 0.f, ay = 0.f;
-  float2 cj = cv;
-  if (j >= 0) cj = bh_live(p, j, plo, phi, pend);
+  float2 cj[BH_LPL];
+#pragma unroll
+  for (int u = 0; u < BH_LPL; ++u) cj[u] = j[u] >= 0 ? bh_live(p, j[u], plo, phi, pend) : cv;
   if (!split) bh_attr_lane(p, k0, k1, cv, plo, phi, pend, ax, ay);
-  if (j >= 0) {
-    const float dx = cj.x - cv.x, dy = cj.y - cv.y;
-    const float d2 = fmaf(dx, dx, dy * dy);
-    if (d2 > 0.f) {
-      const float r = bh_rep_weight(p, d2);
-      fx = fmaf(-r, dx, fx);
-      fy = fmaf(-r, dy, fy);
+#pragma unroll
+  for (int u = 0; u < BH_LPL; ++u)
+    if (j[u] >= 0) {
+      const float dx = cj[u].x - cv.x, dy = cj[u].y - cv.y;
+      const float d2 = fmaf(dx, dx, dy * dy);
+      if (d2 > 0.f) {
+        const float r = bh_rep_weight(p, d2);
+        fx = fmaf(-r, dx, fx);
+        fy = fmaf(-r, dy, fy);
+      }
     }
-  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     fx += __shfl_xor_sync(0xffffffffu, fx, o);
@@ -870,6 +885,149 @@ __device__ __forceinline__ float2 bh_force_pre(const BHKParams &p, int v, float2
     ay = g.y;
   }
   return make_float2(fx + cf.x + ax, fy + cf.y + ay);
+}
+
+// Everything about a batch vertex that is constant within the iteration --
+// its own coordinate (it does not move before its batch, reading B5), its
+// precomputed cell sum and leaf list, its row bounds and first 32 neighbour
+// ids -- loaded for the warp's first vertex of the NEXT batch between the
+// arrival at the grid barrier and the wait, so that after the barrier only
+// the live coordinates (leaf vertices, neighbours) are one L2 trip away.
+// Before: four dependent trips per batch after three of the item pass.
+struct BHPre {
+  int valid, v, nl, j[BH_LPL], ip0, ip1, k0, k1, col;
+  float2 cv, cf;
+};
+__device__ __forceinline__ void bh_prefetch(const BHKParams &p, int lo, int bt, BHPre &o) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = warp * gridDim.x + blockIdx.x;
+  o.valid = p.precompute && i < bt;
+  if (!o.valid) return;
+  const int v = lo + i;
+  o.v = v;
+  o.cv = __ldcg(p.xy + v);
+  o.nl = __ldcg(p.nleaf + v);
+#pragma unroll
+  for (int u = 0; u < BH_LPL; ++u)  // entries >= nl: masked by the user
+    o.j[u] = __ldcg(p.leafv + (size_t)v * BH_LCAP + lane + 32 * u);
+  o.ip0 = __ldg(p.item_ptr + v);
+  o.ip1 = __ldg(p.item_ptr + v + 1);
+  o.k0 = __ldg(p.rowptr + v);
+  o.k1 = __ldg(p.rowptr + v + 1);
+  o.cf = __ldcg(p.cellf + v);
+  o.col = o.k0 + lane < o.k1 ? __ldg(p.colidx + o.k0 + lane) : -1;
+}
+// The edge-parallel pass over the split rows of a batch (layout mode): split
+// item s of the batch goes to warp BH_NW-1 - s / G of CTA s mod G -- the warps
+// that hold no batch vertex while b <= G BH_NW / 2 -- so the pass runs beside
+// the forces instead of before them.  A warp's first item of the NEXT batch
+// (ids, row range, the vertex's own coordinate, its <= BL_ECH neighbour ids)
+// is prefetched with the batch vertex's inputs (bh_prefetch).
+#define BH_IPL (BL_ECH / 32)
+struct BHItemPre {
+  int valid, sib, sie;  // the batch's split items [sib, sie)
+  int4 it;              // this warp's first one: {item, vertex, k0, k1}
+  int col[BH_IPL];
+  float2 cv;
+};
+__device__ __forceinline__ int bh_item_rank() {
+  return (BH_NW - 1 - (int)(threadIdx.x >> 5)) * gridDim.x + blockIdx.x;
+}
+__device__ __forceinline__ void bh_prefetch_item(const BHKParams &p, int lo, int bt, BHItemPre &o) {
+  const int lane = threadIdx.x & 31;
+  o.sib = __ldg(p.split_ptr + lo);
+  o.sie = __ldg(p.split_ptr + lo + bt);
+  const int s = o.sib + bh_item_rank();
+  o.valid = s < o.sie;
+  if (!o.valid) return;
+  o.it = __ldg(p.sitems + s);
+  o.cv = __ldcg(p.xy + o.it.y);
+#pragma unroll
+  for (int u = 0; u < BH_IPL; ++u) {
+    const int k = o.it.z + lane + 32 * u;
+    o.col[u] = k < o.it.w ? __ldg(p.colidx + k) : -1;
+  }
+}
+// publish one item's partial (release flag stamped with the batch)
+__device__ __forceinline__ void bh_item_publish(const BHKParams &p, int a, float fx, float fy,
+                                                unsigned stamp) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    p.attr[a] = make_float2(fx, fy);
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.aflag + a), "r"(stamp) : "memory");
+  }
+}
+__device__ __forceinline__ void bh_items_batch(const BHKParams &p, const BHItemPre &o, unsigned stamp,
+                                               int plo, int phi, const float2 *pend) {
+  const int GW = gridDim.x * BH_NW;
+  int s = o.sib + bh_item_rank();
+  if (o.valid) {  // the prefetched item: only the live coordinates are loaded here
+    float2 cj[BH_IPL];
+#pragma unroll
+    for (int u = 0; u < BH_IPL; ++u)
+      cj[u] = o.col[u] >= 0 ? bh_live(p, o.col[u], plo, phi, pend) : o.cv;
+    float fx = 0.f, fy = 0.f;
+#pragma unroll
+    for (int u = 0; u < BH_IPL; ++u)
+      if (o.col[u] >= 0) bh_attr_term(p, cj[u], o.cv, fx, fy);
+    bh_item_publish(p, o.it.x, fx, fy, stamp);
+    s += GW;
+  }
+  for (; s < o.sie; s += GW) {
+    const int4 it = __ldg(p.sitems + s);
+    float fx = 0.f, fy = 0.f;
+    bh_attr_lane(p, it.z, it.w, __ldcg(p.xy + it.y), plo, phi, pend, fx, fy);
+    bh_item_publish(p, it.x, fx, fy, stamp);
+  }
+}
+
+// bh_force_pre on prefetched inputs: the same terms in the same order.
+__device__ __forceinline__ float2 bh_force_pre2(const BHKParams &p, const BHPre &o, int plo, int phi,
+                                                const float2 *pend, unsigned stamp) {
+  const int lane = threadIdx.x & 31;
+  const bool split = o.ip1 - o.ip0 > 1;
+  const float2 cv = o.cv;
+  float fx = 0.f, fy = 0.f, ax = 0.f, ay = 0.f;
+  int j[BH_LPL];
+  float2 cj[BH_LPL], cn = cv;
+#pragma unroll
+  for (int u = 0; u < BH_LPL; ++u) {
+    j[u] = lane + 32 * u < o.nl ? o.j[u] : -1;
+    cj[u] = j[u] >= 0 ? bh_live(p, j[u], plo, phi, pend) : cv;
+  }
+  if (!split && o.col >= 0) cn = bh_live(p, o.col, plo, phi, pend);
+  if (!split) {
+    if (o.col >= 0) bh_attr_term(p, cn, cv, ax, ay);
+    bh_attr_lane(p, o.k0 + 32, o.k1, cv, plo, phi, pend, ax, ay);
+  }
+#pragma unroll
+  for (int u = 0; u < BH_LPL; ++u)
+    if (j[u] >= 0) {
+      const float dx = cj[u].x - cv.x, dy = cj[u].y - cv.y;
+      const float d2 = fmaf(dx, dx, dy * dy);
+      if (d2 > 0.f) {
+        const float r = bh_rep_weight(p, d2);
+        fx = fmaf(-r, dx, fx);
+        fy = fmaf(-r, dy, fy);
+      }
+    }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o2);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o2);
+    ax += __shfl_xor_sync(0xffffffffu, ax, o2);
+    ay += __shfl_xor_sync(0xffffffffu, ay, o2);
+  }
+  if (split) {
+    const float2 g = bh_attr_gather(p, o.v, stamp);
+    ax = g.x;
+    ay = g.y;
+  }
+  return make_float2(fx + o.cf.x + ax, fy + o.cf.y + ay);
 }
 
 // Fixed-order sum of the G per-CTA fp64 energies by one warp (identical in
@@ -915,6 +1073,15 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
       pf.mark(7);
     }
     double e_acc = 0.0;
+    const int pre_on = p.pre2;
+    BHPre pre;
+    pre.valid = 0;
+    BHItemPre ipre;
+    ipre.valid = 0;
+    if (pre_on) {
+      bh_prefetch(p, 0, min(p.b, p.n), pre);
+      bh_prefetch_item(p, 0, min(p.b, p.n), ipre);
+    }
     for (int t = 0; t < p.nb; ++t) {
       const int lo = t * p.b, bt = min(p.b, p.n - lo);
       float2 *pend_t = p.pend + (size_t)((batches & 1) * p.b);
@@ -924,17 +1091,32 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
         p.xy[plo + i] = __ldcg(pend_prev + i);
       // F: forces of batch t against frozen coordinates (lines 13-20), then
       // the update (lines 21-24) into pend.  Long CSR rows first, edge-
-      // parallel over all warps (no warp waits before its items are done).
+      // parallel over all warps (no warp waits before its items are done);
+      // skipped when the batch has no split row.
       const unsigned stamp = (unsigned)batches + 1u;
-      bh_attr_items(p, lo, lo + bt, gw, GW, stamp, plo, phi, pend_prev);
+#ifdef BH_FINE_TS
+      pf.mark(0);  // commit
+#endif
+      if (pre_on) bh_items_batch(p, ipre, stamp, plo, phi, pend_prev);
+      else bh_attr_items(p, lo, lo + bt, gw, GW, stamp, plo, phi, pend_prev);
+#ifdef BH_FINE_TS
+      pf.mark(1);  // item pass
+#endif
       // batch entry i -> CTA i mod G, warp i / G: the queries spread over
       // all SMs (b = 1024 on 148 SMs: ~7 concurrent traversals per SM)
       for (int i = warp * G + c; i < bt; i += GW) {
         const int v = lo + i;
-        const float2 cv = __ldcg(p.xy + v);
-        const int nl = p.precompute ? __ldcg(p.nleaf + v) : -1;
-        const float2 f = nl >= 0 ? bh_force_pre(p, v, cv, nl, plo, phi, pend_prev, stamp)
-                                 : bh_force_warp(p, sh, v, cv, plo, phi, pend_prev, stamp, vis);
+        const bool fast = pre.valid && i == warp * G + c && pre.nl >= 0;
+        float2 cv, f;
+        if (fast) {
+          cv = pre.cv;
+          f = bh_force_pre2(p, pre, plo, phi, pend_prev, stamp);
+        } else {
+          cv = __ldcg(p.xy + v);
+          const int nl = p.precompute ? __ldcg(p.nleaf + v) : -1;
+          f = nl >= 0 ? bh_force_pre(p, v, cv, nl, plo, phi, pend_prev, stamp)
+                      : bh_force_warp(p, sh, v, cv, plo, phi, pend_prev, stamp, vis);
+        }
         if (lane == 0) {
           const double q = (double)f.x * f.x + (double)f.y * f.y;
           float2 nv = cv;
@@ -947,6 +1129,9 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
           e_acc += q;
         }
       }
+#ifdef BH_FINE_TS
+      pf.mark(2);  // force + update of this warp's vertices
+#endif
       ++batches;
       const bool last = t == p.nb - 1;
       const bool mb = p.max_batches > 0 && batches >= p.max_batches;
@@ -961,7 +1146,25 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
         }
       }
       pf.mark(5);
-      bl_grid_sync(p.bar, bar_target, unit_dummy_ptr);
+      // grid barrier, split: the next batch's iteration-constant inputs are
+      // loaded between the arrival and the wait
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        bar_target += gridDim.x;
+        asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar)
+                     : "memory");
+      }
+      pre.valid = 0;
+      ipre.valid = 0;
+      if (pre_on && !last && !mb) {
+        const int lo2 = lo + p.b, bt2 = min(p.b, p.n - lo2);
+        bh_prefetch(p, lo2, bt2, pre);
+        bh_prefetch_item(p, lo2, bt2, ipre);
+      }
+      if (threadIdx.x == 0)
+        while ((int)(bl_ld_acquire(p.bar) - bar_target) < 0) {
+        }
+      __syncthreads();
       pf.mark(6);
       plo = lo;
       phi = lo + bt;

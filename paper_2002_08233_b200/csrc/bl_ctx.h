@@ -20,6 +20,8 @@ struct bl_ctx {
   // device CSR + items
   int *d_rowptr = nullptr, *d_colidx = nullptr;
   int *d_item_ptr = nullptr, *d_item_v = nullptr, *d_item_k0 = nullptr;
+  int *d_split_ptr = nullptr;  // items of split vertices below v (BatchLayoutBH)
+  int4 *d_sitems = nullptr;    // those items: {item, vertex, k0, k1}
   std::vector<int> item_ptr;  // host copy (per-batch maxima)
   std::vector<int> rowptr_host;  // host copy of rowptr (entry ranges)
   int *d_coo_row = nullptr;      // COO row id per CSR entry (metric helpers)

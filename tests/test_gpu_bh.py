@@ -242,3 +242,30 @@ def test_precompute_off_matches(monkeypatch):
             torch.cuda.synchronize()
             out[pre] = d.cpu().numpy()
     assert_positions_close(out["1"], out["0"].astype(np.float64), what="precompute on/off")
+
+
+@pytest.mark.parametrize("name,iters", [("C4", 2), ("C2", 3), ("C5", 1)])
+def test_prefetch_across_the_barrier_is_bitwise_neutral(name, iters, monkeypatch):
+    """BL_BH_PRE2 (default on): a batch vertex's iteration-constant inputs are
+    loaded between the arrival at the grid barrier and the wait, and batches
+    without split rows skip the item pass -- the same terms in the same order,
+    so positions, energy trace and visit count are bitwise those of the
+    unprefetched loop (BL_BH_PRE2=0).  C4 / C2 have split (hub) rows in their
+    first batches and none later."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g, xy0, cfg = build_config(name)
+    out = {}
+    for pre2 in ("1", "0"):
+        monkeypatch.setenv("BL_BH_PRE2", pre2)
+        with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+            d = torch.from_numpy(xy0.copy()).cuda()
+            lay.layout_device(d, iters=iters, batch=cfg.batch, **_bh())
+            torch.cuda.synchronize()
+            _, tr, done = lay.energy(trace_len=iters)
+            out[pre2] = (d.cpu().numpy(), tr, done, bl.bl_last_visits(lay.h))
+    assert out["1"][2] == out["0"][2] == iters
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert out["1"][3] == out["0"][3]
