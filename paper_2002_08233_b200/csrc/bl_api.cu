@@ -362,6 +362,7 @@ extern "C" void bl_destroy(bl_ctx *h) {
   cudaFree(h->d_visits);
   cudaFree(h->d_attr_bh);
   cudaFree(h->d_aflag);
+  cudaFree(h->d_attr_ll);
   cudaFree(h->d_cellf);
   cudaFree(h->d_nleaf);
   cudaFree(h->d_leafv);
@@ -679,6 +680,7 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
     ALLOC(h->d_visits, G);
     ALLOC(h->d_attr_bh, std::max(1, h->n_items));
     ALLOC(h->d_aflag, std::max(1, h->n_items));
+    ALLOC(h->d_attr_ll, std::max(1, h->n_items));
     ALLOC(h->d_cellf, n);
     ALLOC(h->d_nleaf, n);
     ALLOC(h->d_leafv, (size_t)n * BH_LCAP);
@@ -735,6 +737,7 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   k.item_k0 = h->d_item_k0;
   k.attr = h->d_attr_bh;
   k.aflag = h->d_aflag;
+  k.attr_ll = h->d_attr_ll;
   k.cellf = h->d_cellf;
   k.nleaf = h->d_nleaf;
   k.leafv = h->d_leafv;
@@ -759,6 +762,8 @@ static bl_status launch_bh(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStre
   if (!forces_mode) BL_CUDA(h, cudaMemsetAsync(h->d_iters_done, 0, sizeof(int), st));
   BL_CUDA(h, cudaMemsetAsync(h->d_visits, 0, sizeof(unsigned long long) * G, st));
   BL_CUDA(h, cudaMemsetAsync(h->d_aflag, 0, sizeof(unsigned) * std::max(1, h->n_items), st));
+  if (!forces_mode && k.pre2)
+    BL_CUDA(h, cudaMemsetAsync(h->d_attr_ll, 0, sizeof(uint4) * std::max(1, h->n_items), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(bl_bh_threads()), args, smem, st));
   h->launches = 1;

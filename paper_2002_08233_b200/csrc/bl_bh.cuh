@@ -91,6 +91,10 @@ struct BHKParams {
   const int4 *sitems;          // those items in vertex order: {item, vertex, k0, k1}
   float2 *attr;                // [n_items]
   unsigned *aflag;             // [n_items]
+  uint4 *attr_ll;              // [n_items] layout mode with pre2: {fx bits, stamp, fy bits,
+                               // stamp} -- two 8-byte words that each carry their own flag
+                               // (no release fence between value and flag: one L2 trip less
+                               // on the split vertex's critical path)
   unsigned long long *prof;    // optional phase profile (BL_PROFILE=1)
 };
 
@@ -709,13 +713,35 @@ __device__ __forceinline__ void bh_attr_items(const BHKParams &p, int vlo, int v
 }
 
 // Sum of the published item partials of split vertex v (waits for them).
+__device__ __forceinline__ uint2 bh_ld_relaxed_v2(const void *q) {
+  uint2 r;
+  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(q) : "memory");
+  return r;
+}
+__device__ __forceinline__ void bh_st_relaxed_v2(void *q, unsigned a, unsigned b) {
+  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(q), "r"(a), "r"(b) : "memory");
+}
 __device__ __forceinline__ float2 bh_attr_gather(const BHKParams &p, int v, unsigned stamp) {
   const int lane = threadIdx.x & 31;
   const int a0 = __ldg(p.item_ptr + v), a1 = __ldg(p.item_ptr + v + 1);
   float fx = 0.f, fy = 0.f;
+  const bool ll = p.pre2 && !p.forces_mode;
   for (int a = a0 + lane; a < a1; a += 32) {
-    while (bl_ld_acquire(p.aflag + a) != stamp) __nanosleep(20);
-    const float2 q = __ldcg(p.attr + a);
+    float2 q;
+    if (ll) {
+      // each 8-byte word is written by one store: (value, stamp) arrive together
+      uint2 w0, w1;
+      for (;;) {
+        w0 = bh_ld_relaxed_v2(&p.attr_ll[a].x);
+        w1 = bh_ld_relaxed_v2(&p.attr_ll[a].z);
+        if (w0.y == stamp && w1.y == stamp) break;
+        __nanosleep(20);
+      }
+      q = make_float2(__uint_as_float(w0.x), __uint_as_float(w1.x));
+    } else {
+      while (bl_ld_acquire(p.aflag + a) != stamp) __nanosleep(20);
+      q = __ldcg(p.attr + a);
+    }
     fx += q.x;
     fy += q.y;
   }
@@ -957,8 +983,8 @@ __device__ __forceinline__ void bh_item_publish(const BHKParams &p, int a, float
     fy += __shfl_xor_sync(0xffffffffu, fy, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    p.attr[a] = make_float2(fx, fy);
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.aflag + a), "r"(stamp) : "memory");
+    bh_st_relaxed_v2(&p.attr_ll[a].x, __float_as_uint(fx), stamp);
+    bh_st_relaxed_v2(&p.attr_ll[a].z, __float_as_uint(fy), stamp);
   }
 }
 __device__ __forceinline__ void bh_items_batch(const BHKParams &p, const BHItemPre &o, unsigned stamp,
@@ -1086,9 +1112,18 @@ __device__ void bh_run_batches(const BHKParams &p, BHShared &sh, unsigned &bar_t
       const int lo = t * p.b, bt = min(p.b, p.n - lo);
       float2 *pend_t = p.pend + (size_t)((batches & 1) * p.b);
       const float2 *pend_prev = p.pend + (size_t)(((batches - 1) & 1) * p.b);
-      // commit batch t-1 (nobody reads its xy entries in this phase)
-      for (int i = c * NT + threadIdx.x; i < phi - plo; i += G * NT)
-        p.xy[plo + i] = __ldcg(pend_prev + i);
+      // commit batch t-1 (nobody reads its xy entries in this phase): by the
+      // upper half of every CTA's warps, which hold no batch vertex while
+      // b <= G BH_NW / 2 (CTAs 0 and 1 alone used to do it, ahead of their
+      // own vertices' forces: 0.4 us on the batch's critical path)
+      if (pre_on) {
+        for (int i = c * (NT / 2) + (int)threadIdx.x - NT / 2; threadIdx.x >= NT / 2 && i < phi - plo;
+             i += G * (NT / 2))
+          p.xy[plo + i] = __ldcg(pend_prev + i);
+      } else {
+        for (int i = c * NT + threadIdx.x; i < phi - plo; i += G * NT)
+          p.xy[plo + i] = __ldcg(pend_prev + i);
+      }
       // F: forces of batch t against frozen coordinates (lines 13-20), then
       // the update (lines 21-24) into pend.  Long CSR rows first, edge-
       // parallel over all warps (no warp waits before its items are done);

@@ -75,6 +75,7 @@ struct bl_ctx {
   bool last_bh = false;
   float2 *d_attr_bh = nullptr;
   unsigned *d_aflag = nullptr;
+  uint4 *d_attr_ll = nullptr;  // BH split-row partials with in-word flags (layout mode)
   float2 *d_cellf = nullptr;  // BH per-iteration precomputation
   int *d_nleaf = nullptr, *d_leafv = nullptr;
   // checked builds (-DBL_CHECKED): violation record and phase stamps
