@@ -264,6 +264,8 @@ extern "C" bl_status bl_create(int32_t n, const int32_t *rowptr, const int32_t *
     h->item_ptr[v + 1] = h->item_ptr[v] + (deg + BL_ECH - 1) / BL_ECH;
   }
   h->n_items = h->item_ptr[n];
+  h->n_long_rows = 0;  // rows of more than BL_LCOOP entries (latency driver's cooperative walk)
+  for (int32_t v = 0; v < n; ++v) h->n_long_rows += rowptr[v + 1] - rowptr[v] > BL_LCOOP ? 1 : 0;
   // BatchLayoutBH: the items of split vertices (rows of more than one item)
   // as one list in vertex order, {item, vertex, k0, k1} each, with split_ptr[v]
   // = the number of them below vertex v: a batch's edge-parallel pass walks
@@ -624,6 +626,12 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // sequential batches, whose hubs sit in the first batches); with relabelled
   // randomised batches every batch holds hub rows (BL_LONG8 overrides)
   k.long8 = env_int("BL_LONG8", (k.pipelined == 2 || rl) ? 1 : 0);
+  // latency driver: long rows walked by all updater warps together where the
+  // graph has enough of them to meet one in most batches (>= one row of more
+  // than BL_LCOOP entries per 8 batches; measured same box: C4 1,157 -> 1,295
+  // it/s, relabelled C4 1.29 -> 0.94 ms per iteration; the hub-free configs
+  // keep the plain instance, which the walk would cost 6 %)
+  k.lcoop = env_int("BL_LCOOP", (long long)h->n_long_rows * 8 >= k.nb ? 1 : 0);
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   h->driver_last = forces_mode ? "two-barrier"

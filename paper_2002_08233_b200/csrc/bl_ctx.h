@@ -35,6 +35,7 @@ struct bl_ctx {
   unsigned *d_la_bar = nullptr;  // grid-barrier counter of bla_kernel (monotone)
   unsigned la_bar_base = 0;
   int n_items = 0;
+  int n_long_rows = 0;  // rows of more than BL_LCOOP entries
   // scratch
   float2 *d_part = nullptr;
   size_t part_cap = 0;  // float2 elements

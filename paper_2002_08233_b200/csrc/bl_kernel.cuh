@@ -130,6 +130,8 @@ struct BLKParams {
                          // without CTA-wide barriers between phases (bl_run_async)
   int part_nbuf;         // part buffers (2: pipelined, 3: async)
   int afence_gpu;        // async: GPU-scope fences in every task (debug, BL_AFENCE=1)
+  int lcoop;             // latency driver: rows of > BL_LCOOP entries walked by all updater
+                         // warps of the CTA together (bl_long_row_part)
   int long8;             // update tasks walk long CSR rows 256 entries per round (8 gathers
                          // in flight per lane): the async driver always; the others when
                          // every batch holds hub rows (relabelled randomised batches)
@@ -965,6 +967,10 @@ struct BLShared {
   int l_join[2];               // updater warps that finished phase q's update
   int l_unit[2], l_exit[2], l_gen[2], l_tiles[2];
   int l_tdone[2][BL_NTT_MAX];
+  // long rows (> BL_LCOOP entries) of the CTA's members, walked by all updater
+  // warps together: row start / degree per member, one partial per (member, warp)
+  int l_k0[BL_NW_MAX / 2], l_deg[BL_NW_MAX / 2];
+  float2 l_lpart[BL_NW_MAX / 2][BL_NW_MAX / 2];
 #ifdef BL_PHASE_TS
   // critical-path timestamps (profiling builds, -DBL_PHASE_TS; they cost ~3 %
   // at C5 even when disabled at run time, so they are compiled out by
@@ -1044,9 +1050,12 @@ __device__ __forceinline__ void bl_chk_nb(const BLKParams &p, int q, int j, int 
 }
 
 // Update of one owned vertex v of batch q (warp-cooperative); ||f||^2 -> *eq.
+// apart != nullptr: the row's attraction was computed by napart warps
+// (bl_long_row_part), summed here in warp order.
 __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, double stepd,
                                               float4 *src4, double *eq, const int *srow,
-                                              int sdeg) {
+                                              int sdeg, const float2 *apart = nullptr,
+                                              int napart = 0) {
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31;
   const int lo = (q % p.nb) * p.b;
   const int local = v - lo;
@@ -1069,7 +1078,7 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     cj_st = (j_st >= plo && j_st < phi) ? __ldcg(pend_prev + (j_st - plo)) : __ldcg(p.xy + j_st);
   }
   int k0 = 0, k1 = 0;
-  if (!srow) {
+  if (!srow && !apart) {
     k0 = __ldg(p.rowptr + v);
     k1 = __ldg(p.rowptr + v + 1);
   }
@@ -1160,7 +1169,13 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
       }
     }
   };
-  if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});  // branch hoisted out of the loop
+  if (apart) {
+    if (lane == 0)
+      for (int w = 0; w < napart; ++w) {
+        sx += apart[w].x;
+        sy += apart[w].y;
+      }
+  } else if (p.amode == 0 && p.rmode == 0) scan_row(std::true_type{});  // branch hoisted out of the loop
   else scan_row(std::false_type{});
   rx = bl_warp_sum0(rx);
   ry = bl_warp_sum0(ry);
@@ -1184,6 +1199,58 @@ __device__ __forceinline__ void bl_update_one(const BLKParams &p, int q, int v, 
     }
     *eq = qq;
   }
+}
+
+// Latency driver: a member's long CSR row [k0, k0 + deg) walked by the CTA's U
+// updater warps together -- warp w takes the 256-entry chunks w, w + U, ...
+// (8 gathers in flight per lane), its partial attraction (+ neighbour
+// correction) sum goes to lane 0.  Same terms as bl_update_one's row scan;
+// the owner adds the U partials in warp order.
+#define BL_LCOOP 256
+__device__ __forceinline__ float2 bl_long_row_part(const BLKParams &p, int q, int k0, int deg,
+                                                   float2 ci, int w, int U) {
+  const int lane = threadIdx.x & 31;
+  int plo = 0, phi = 0;
+  const float2 *pend_prev = p.pend + (size_t)((q - 1) & 1) * p.b;
+  if (q >= 1) {
+    plo = ((q - 1) % p.nb) * p.b;
+    phi = min(plo + p.b, p.n);
+  }
+  const float rep = (p.flags & 1u) ? 0.f : p.ck2;
+  const int k1 = k0 + deg;
+  float sx = 0.f, sy = 0.f;
+  auto walk = [&](auto fast) {
+    for (int base = k0 + w * 256; base < k1; base += U * 256) {
+      int jj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = base + lane + 32 * u;
+        jj[u] = k < k1 ? __ldg(p.colidx + k) : -1;
+      }
+      float2 cj[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = jj[u];
+        cj[u] = j < 0 ? ci : (j >= plo && j < phi) ? __ldcg(pend_prev + (j - plo)) : __ldcg(p.xy + j);
+        if (BL_CHK_ON && j >= 0) bl_chk_nb(p, q, j, plo, phi);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (jj[u] < 0) continue;
+        const float dx = cj[u].x - ci.x, dy = cj[u].y - ci.y;
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, BL_EPS2));
+        const float rs = bl_rsqrt(d2);
+        const float coef = bl_model_coef<decltype(fast)::value>(p, d2, rs, rep);
+        sx = fmaf(coef, dx, sx);
+        sy = fmaf(coef, dy, sy);
+      }
+    }
+  };
+  if (p.amode == 0 && p.rmode == 0) walk(std::true_type{});
+  else walk(std::false_type{});
+  sx = bl_warp_sum0(sx);
+  sy = bl_warp_sum0(sy);
+  return make_float2(sx, sy);
 }
 
 // Phase geometry shared by all warps of a CTA.
@@ -1888,7 +1955,7 @@ __device__ __forceinline__ void bl_run_async(const BLKParams &p, float4 *src4, f
 //             every target in fixed order -> part, arrives at barrier q.
 // Same values and summation order as the asynchronous driver's (the clean
 // sub-ranges in order, then the dirty one).  Needs nb >= 4.
-template <int T, int TP>
+template <int T, int TP, bool LCOOP>
 __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, float2 *tgt,
                                            float2 *red, BLShared &sh) {
   const int G = gridDim.x, c = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2050,6 +2117,10 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
         const int k0 = __ldg(p.rowptr + v);
         deg = __ldg(p.rowptr + v + 1) - k0;
         if (deg <= 32 && lane < deg) myrow[lane] = __ldg(p.colidx + k0 + lane);
+        if (LCOOP && lane == 0) {  // for the cooperative walk of long rows (read after ubar)
+          sh.l_k0[warp] = k0;
+          sh.l_deg[warp] = deg;
+        }
         __syncwarp();
       }
       if (warp == 0) {
@@ -2081,9 +2152,28 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
       t_det = clock64();
 #endif
       bl_jitter(p, 32);
-      if (vs.stop_flag == 0 && warp < m)
-        bl_update_one(p, q - 1, v0 + warp * G, step_u, src4, &sh.e_task[warp],
-                      deg <= 32 ? myrow : nullptr, deg <= 32 ? deg : 0);
+      // long rows of this CTA's members: all U updater warps walk them
+      // together (p.lcoop; a hub's update is the batch's critical path)
+      bool coop = false;
+      if (LCOOP && vs.stop_flag == 0) {
+        for (int t = 0; t < m; ++t) {
+          const int dt = vs.l_deg[t];
+          if (dt <= BL_LCOOP) continue;
+          coop = true;
+          const float2 ci = bl_src_get(src4, (v0 + t * G - c) / G);
+          const float2 f = bl_long_row_part(p, q - 1, vs.l_k0[t], dt, ci, warp, U);
+          if (lane == 0) sh.l_lpart[t][warp] = f;
+        }
+        if (coop) ubar();  // uniform: every updater warp sees the same degrees
+      }
+      if (vs.stop_flag == 0 && warp < m) {
+        if (LCOOP && coop && deg > BL_LCOOP)
+          bl_update_one(p, q - 1, v0 + warp * G, step_u, src4, &sh.e_task[warp], nullptr, 0,
+                        sh.l_lpart[warp], U);
+        else
+          bl_update_one(p, q - 1, v0 + warp * G, step_u, src4, &sh.e_task[warp],
+                        deg <= 32 ? myrow : nullptr, deg <= 32 ? deg : 0);
+      }
     }
     ubar();  // every member of M(q-1) updated (src4, pend, e_task)
 #ifdef BL_PHASE_TS
@@ -2296,7 +2386,10 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
     return;
   }
   if (p.pipelined == 3) {
-    bl_run_lat<T, TP>(p, src4, tgt, red, sh);
+    // two instances: the cooperative long-row walk costs the hub-free configs
+    // 6 % when merely compiled into their loop (measured at C2 / C3)
+    if (p.lcoop) bl_run_lat<T, TP, true>(p, src4, tgt, red, sh);
+    else bl_run_lat<T, TP, false>(p, src4, tgt, red, sh);
     return;
   }
   if (p.pipelined) {
