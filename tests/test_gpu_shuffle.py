@@ -223,3 +223,32 @@ def test_shuffled_driver_and_rejections(monkeypatch):
             with pytest.raises(bl.BLError) as ei:
                 lay.layout_device(d, iters=1, **bad)
             assert ei.value.status == bl.BL_EINVAL
+
+
+@pytest.mark.parametrize("rows,cols,b", [(5, 8, 4), (17, 19, 10), (30, 37, 64), (40, 50, 2)])
+def test_relabelled_small_and_ragged_shapes(rows, cols, b):
+    """Relabelling on graphs smaller than the grid (n < 148 positions: most
+    CTAs of bl_relabel_kernel hold no position), ragged last batches and the
+    smallest even batch: one iteration vs the oracle, driver name, and the
+    seeded run is reproducible bitwise."""
+    import torch
+
+    import paper_2002_08233_b200 as bl
+    g = grid_graph(rows, cols)
+    xy0 = uniform_coords(g.n, 5)
+    p = dict(iters=1, batch=b, shuffle_seed=SEED)
+    with bl.BatchLayout(g.n, g.rowptr, g.colidx) as lay:
+        d = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d, **p)
+        torch.cuda.synchronize()
+        assert bl.bl_driver_name(lay.h).startswith("relabel+")
+        got = d.cpu().numpy()
+        _, tr, done = lay.energy(trace_len=1)
+        d2 = torch.from_numpy(xy0.copy()).cuda()
+        lay.layout_device(d2, **p)
+        torch.cuda.synchronize()
+        assert np.array_equal(d2.cpu().numpy(), got)
+    ref, E, _ = oracle.layout(g.n, g.rowptr, g.colidx, xy0, **p)
+    assert done == 1
+    assert_positions_close(got, ref, POS_TOL, what=f"relabelled {rows}x{cols} b={b}")
+    assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p), what=f"relabelled {rows}x{cols} b={b}")
