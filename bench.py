@@ -490,7 +490,7 @@ def bench_shuffle(args, lay, d_xy0, params, stream, flush, cfg, t_default):
     Default: every iteration relabelled into position space (one extra launch,
     csrc/bl_relabel.cu) and run by the sequential driver; `inkernel` is the
     round-2 first version, randomised inside the two-barrier driver
-    (BL_SHUFFLE_RELABEL=0; still used with tol > 0)."""
+    (BL_SHUFFLE_RELABEL=0)."""
     import paper_2002_08233_b200 as bl
     steps = max(2, min(args.steps, 3))
     t_shuf = _time_layout(lay, d_xy0, dict(params, shuffle_seed=1), stream, flush, steps)

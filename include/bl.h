@@ -94,8 +94,9 @@ typedef struct {
                           evaluate.  BL_ALGO_EXACT only (BL_EINVAL with BH).
                           Each iteration is relabelled into position space
                           (one extra launch) and runs on the sequential
-                          drivers; with tol > 0, or where those do not apply,
-                          the two-barrier driver randomises in the kernel
+                          drivers (tol > 0 is tested on the device between
+                          the launches); where those do not apply the
+                          two-barrier driver randomises in the kernel
                                                               */
 } bl_params;
 

@@ -444,6 +444,7 @@ struct BLRelabelRun {
   int probe;      // in: 1 = no launch, out: pipelined
   int pipelined;  // out: BLKParams::pipelined of this (n, b)
   int it;         // iteration (checked builds: the violation record is zeroed at it = 0 only)
+  const int *stop_in;  // tol > 0: device flag that turns the launch into a no-op
 };
 static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
                         int forces_mode, int first, int count, float2 *f_out,
@@ -527,6 +528,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   k.e_cta = h->d_e_cta;
   k.energy = rl ? rl->energy : h->d_energy;
   k.iters_done = rl ? rl->iters_done : h->d_iters_done;
+  k.stop_in = rl ? rl->stop_in : nullptr;
   k.bar = h->d_bar;
   k.f_out = f_out;
   k.prof = h->d_prof;
@@ -900,16 +902,18 @@ extern "C" bl_status bl_last_visits(bl_ctx *h, unsigned long long *visits) {
 // iteration is one relabel launch + one plain launch of the layout kernel in
 // position space, with whatever sequential driver (asynchronous, latency,
 // pipelined) the size takes.  Taken when the whole-GPU kernel would run one of
-// those drivers and the call has no convergence rule (tol > 0 is decided on
-// the device between iterations: the in-kernel randomisation of the
-// two-barrier driver keeps it); BL_SHUFFLE_RELABEL=0 turns it off.
+// those drivers; BL_SHUFFLE_RELABEL=0 turns it off.  tol > 0 stays a
+// device-side decision: the relabel launch of iteration it >= 2 tests
+// |E[it-1] - E[it-2]| < tol in every CTA alike, books iters_done = it and
+// sets a flag that makes the remaining launches of the call no-ops (the
+// layout kernel checks BLKParams::stop_in first); the single-cluster kernel
+// has no such check, so tol > 0 takes the whole-GPU kernel.
 // max_batches: the iteration that exhausts the budget gets the rest of it.  The Step of iteration it is
 // step0 cooling^it by the same repeated fp64 product as in the kernel.
 static bl_status layout_relabel(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_t st,
                                 bool *used) {
   *used = false;
-  if (!p->shuffle_seed || p->algo != BL_ALGO_EXACT || p->tol != 0.0 ||
-      env_int("BL_SHUFFLE_RELABEL", 1) == 0)
+  if (!p->shuffle_seed || p->algo != BL_ALGO_EXACT || env_int("BL_SHUFFLE_RELABEL", 1) == 0)
     return BL_OK;
   bl_status s = bl_relabel_alloc(h);
   if (s != BL_OK) return s;
@@ -917,9 +921,11 @@ static bl_status layout_relabel(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
   q.iters = 1;
   q.shuffle_seed = 0;
   q.max_batches = 0;
-  BLRelabelRun rl{h->d_rowptrP, h->d_colidxP, nullptr, h->d_rl_iters, 1, 0, 0};
+  q.tol = 0.0;  // the stop rule runs between the launches
+  const bool tol_stop = p->tol > 0.0;
+  BLRelabelRun rl{h->d_rowptrP, h->d_colidxP, nullptr, h->d_rl_iters, 1, 0, 0, nullptr};
   bool cluster = false;
-  if ((s = launch_cluster(h, h->d_xyP, &q, st, &cluster, &rl)) != BL_OK) return s;
+  if (!tol_stop && (s = launch_cluster(h, h->d_xyP, &q, st, &cluster, &rl)) != BL_OK) return s;
   if (!cluster) {
     if ((s = launch(h, h->d_xyP, &q, st, 0, 0, 0, nullptr, &rl)) != BL_OK) return s;
     if (!rl.pipelined) return BL_OK;
@@ -928,6 +934,8 @@ static bl_status layout_relabel(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
   int shuf_h = 1;
   while ((1LL << (2 * shuf_h)) < (long long)h->n) ++shuf_h;
   rl.probe = 0;
+  rl.stop_in = tol_stop ? h->d_rl_stop : nullptr;
+  if (tol_stop) BL_CUDA(h, cudaMemsetAsync(h->d_rl_stop, 0, sizeof(int), st));
   double step = p->step0;
   int launches = 0, done = 0;
   const int b = std::min(p->batch, h->n);
@@ -935,7 +943,7 @@ static bl_status layout_relabel(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
   for (int it = 0; it < p->iters; ++it) {
     const long long left = p->max_batches > 0 ? p->max_batches - it * nb : nb + 1;
     if ((s = bl_relabel_launch(h, d_xy, (unsigned long long)p->shuffle_seed, shuf_h, it, it > 0,
-                               st)) != BL_OK)
+                               p->tol, st)) != BL_OK)
       return s;
     q.step0 = step;
     q.max_batches = left <= nb ? (int)left : 0;  // the budget ends inside this iteration
@@ -949,7 +957,7 @@ static bl_status layout_relabel(bl_ctx *h, float2 *d_xy, const bl_params *p, cud
     done = it + 1;
     step = step * p->cooling;
   }
-  if ((s = bl_unrelabel_launch(h, d_xy, done, st)) != BL_OK) return s;
+  if ((s = bl_unrelabel_launch(h, d_xy, done, tol_stop, st)) != BL_OK) return s;
   h->launches = launches + 1;
   const std::string d = h->driver_last;
   h->driver_last = d == "async"     ? "relabel+async"

@@ -85,7 +85,7 @@ struct bl_ctx {
   // batch randomisation by relabelling (bl_relabel.cu): pi_it, its inverse and
   // the position-space CSR / coordinates of the current iteration
   int *d_piv = nullptr, *d_inv = nullptr, *d_rowptrP = nullptr, *d_colidxP = nullptr;
-  int *d_rl_sum = nullptr, *d_rl_iters = nullptr;
+  int *d_rl_sum = nullptr, *d_rl_iters = nullptr, *d_rl_stop = nullptr;
   unsigned *d_rl_bar = nullptr;
   float2 *d_xyP = nullptr;
   // quality-metric scratch: grown on first use, kept for the context's life
@@ -132,5 +132,5 @@ int bl_eu_blocks(const bl_ctx *h);  // grid of the edge-uniformity kernel
 bl_status bl_relabel_alloc(bl_ctx *h);
 void bl_relabel_free(bl_ctx *h);
 bl_status bl_relabel_launch(bl_ctx *h, float2 *xy, unsigned long long seed, int shuf_h, int it,
-                            int unperm, cudaStream_t st);
-bl_status bl_unrelabel_launch(bl_ctx *h, float2 *xy, int iters, cudaStream_t st);
+                            int unperm, double tol, cudaStream_t st);
+bl_status bl_unrelabel_launch(bl_ctx *h, float2 *xy, int iters, bool tol_stop, cudaStream_t st);

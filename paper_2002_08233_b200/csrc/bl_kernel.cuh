@@ -130,6 +130,8 @@ struct BLKParams {
                          // without CTA-wide barriers between phases (bl_run_async)
   int part_nbuf;         // part buffers (2: pipelined, 3: async)
   int afence_gpu;        // async: GPU-scope fences in every task (debug, BL_AFENCE=1)
+  const int *stop_in;    // relabelled iterations with tol > 0: the launch is a no-op once a
+                         // previous iteration's convergence test set it (bl_relabel.cu)
   int lcoop;             // latency driver: rows of > BL_LCOOP entries walked by all updater
                          // warps of the CTA together (bl_long_row_part)
   int long8;             // update tasks walk long CSR rows 256 entries per round (8 gathers
@@ -2325,6 +2327,7 @@ __device__ __forceinline__ void bl_run_lat(const BLKParams &p, float4 *src4, flo
 template <int NT, int T, int TP>
 __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
   extern __shared__ float4 bl_smem[];
+  if (p.stop_in && *(const volatile int *)p.stop_in) return;  // uniform: set by an earlier launch
   float4 *src4 = bl_smem;
   float2 *tgt = reinterpret_cast<float2 *>(bl_smem + p.chunk4);
   float2 *red = tgt + 2 * BL_TGT_CAP;

@@ -17,6 +17,14 @@
 struct BLRelabelParams {
   int n, nnz, shuf_h, it, unperm;
   unsigned long long seed;
+  // convergence: before iteration it >= 2, |E[it-1] - E[it-2]| < tol
+  // stops the run -- every CTA takes the same decision from the same two
+  // values; *stop = it + 1 makes every later launch of the call a no-op (the
+  // stopping launch itself must finish its scatter in every CTA, hence the
+  // iteration number: its own CTAs that start late do not take it for theirs)
+  double tol;
+  const double *energy;
+  int *stop, *iters_done;
   const int *rowptr, *colidx;
   int *piv, *inv, *rowptrP, *colidxP, *cta_sum;
   float2 *xy, *xyP;
@@ -57,9 +65,23 @@ __global__ void __launch_bounds__(BLR_NT, 1) bl_relabel_kernel(BLRelabelParams p
   __shared__ int s_total, s_dummy;
   const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   unsigned target = 0;
+  if (p.stop) {  // stopped by an earlier iteration's launch
+    const int sv = *(const volatile int *)p.stop;
+    if (sv != 0 && sv <= p.it) return;
+  }
   // A: the previous iteration's coordinates back to vertex space
   if (p.unperm) {
     for (int i = c * BLR_NT + tid; i < p.n; i += G * BLR_NT) p.xy[__ldcg(p.piv + i)] = __ldcg(p.xyP + i);
+    if (p.tol > 0.0 && p.it >= 2 &&
+        fabs(__ldcg(p.energy + p.it - 1) - __ldcg(p.energy + p.it - 2)) < p.tol) {
+      // (no CTA reads stop after this point in this launch; later launches do)
+      if (c == 0 && tid == 0) {
+        *p.iters_done = p.it;
+        __threadfence();
+        *p.stop = p.it + 1;
+      }
+      return;
+    }
     bl_grid_sync(p.bar, target, &s_dummy);
   }
   const BLPerm P = bl_perm_make(p.seed, p.shuf_h, p.n, p.it, pkey);  // pi_it (R1)
@@ -123,7 +145,8 @@ __global__ void __launch_bounds__(BLR_NT, 1) bl_relabel_kernel(BLRelabelParams p
 
 // the last iteration's coordinates back to vertex space; iters_done <- iters
 __global__ void bl_unrelabel_kernel(int n, const int *piv, const float2 *xyP, float2 *xy,
-                                    int *iters_done, int iters) {
+                                    int *iters_done, int iters, const int *stop) {
+  if (stop && *(const volatile int *)stop) return;  // scattered back by the stopping launch
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     xy[__ldcg(piv + i)] = __ldcg(xyP + i);
   if (blockIdx.x == 0 && threadIdx.x == 0) *iters_done = iters;
@@ -139,7 +162,8 @@ bl_status bl_relabel_alloc(bl_ctx *h) {
       cudaMalloc((void **)&h->d_xyP, sizeof(float2) * n) != cudaSuccess ||
       cudaMalloc((void **)&h->d_rl_sum, sizeof(int) * (size_t)h->num_sms) != cudaSuccess ||
       cudaMalloc((void **)&h->d_rl_bar, sizeof(unsigned)) != cudaSuccess ||
-      cudaMalloc((void **)&h->d_rl_iters, sizeof(int)) != cudaSuccess)
+      cudaMalloc((void **)&h->d_rl_iters, sizeof(int)) != cudaSuccess ||
+      cudaMalloc((void **)&h->d_rl_stop, sizeof(int)) != cudaSuccess)
     return bl_fail(h, BL_ENOMEM, "cudaMalloc relabel buffers");
   return BL_OK;
 }
@@ -153,12 +177,13 @@ void bl_relabel_free(bl_ctx *h) {
   cudaFree(h->d_rl_sum);
   cudaFree(h->d_rl_bar);
   cudaFree(h->d_rl_iters);
+  cudaFree(h->d_rl_stop);
 }
 
 // Position space of iteration `it` from the vertex-space xy (unperm: xyP of
 // the previous iteration is scattered back to xy first).
 bl_status bl_relabel_launch(bl_ctx *h, float2 *xy, unsigned long long seed, int shuf_h, int it,
-                            int unperm, cudaStream_t st) {
+                            int unperm, double tol, cudaStream_t st) {
   BLRelabelParams k{};
   k.n = h->n;
   k.nnz = h->nnz;
@@ -176,6 +201,10 @@ bl_status bl_relabel_launch(bl_ctx *h, float2 *xy, unsigned long long seed, int 
   k.xy = xy;
   k.xyP = h->d_xyP;
   k.bar = h->d_rl_bar;
+  k.tol = tol;
+  k.energy = h->d_energy;
+  k.stop = tol > 0.0 ? h->d_rl_stop : nullptr;
+  k.iters_done = h->d_iters_done;
   BL_CUDA(h, cudaMemsetAsync(h->d_rl_bar, 0, sizeof(unsigned), st));
   void *args[] = {&k};
   BL_CUDA(h, cudaLaunchCooperativeKernel((void *)bl_relabel_kernel, dim3(h->num_sms), dim3(BLR_NT),
@@ -183,9 +212,9 @@ bl_status bl_relabel_launch(bl_ctx *h, float2 *xy, unsigned long long seed, int 
   return BL_OK;
 }
 
-bl_status bl_unrelabel_launch(bl_ctx *h, float2 *xy, int iters, cudaStream_t st) {
+bl_status bl_unrelabel_launch(bl_ctx *h, float2 *xy, int iters, bool tol_stop, cudaStream_t st) {
   bl_unrelabel_kernel<<<h->num_sms, BLR_NT, 0, st>>>(h->n, h->d_piv, h->d_xyP, xy, h->d_iters_done,
-                                                    iters);
+                                                    iters, tol_stop ? h->d_rl_stop : nullptr);
   BL_CUDA(h, cudaGetLastError());
   return BL_OK;
 }

@@ -6,7 +6,7 @@ arithmetic (no shared code: oracle/bl_oracle.c vs csrc/bl_kernel.cuh).
 
 Two GPU realisations: by default every iteration is relabelled
 into position space (csrc/bl_relabel.cu) and runs on the sequential drivers;
-BL_SHUFFLE_RELABEL=0 (or tol > 0) randomises inside the two-barrier driver.
+BL_SHUFFLE_RELABEL=0 randomises inside the two-barrier driver.
 `mode` runs both."""
 import numpy as np
 import pytest
@@ -209,11 +209,10 @@ def test_shuffled_driver_and_rejections(monkeypatch):
         torch.cuda.synchronize()
         assert bl.bl_driver_name(lay.h) == "relabel+async"
         assert bl.bl_last_launch_count(lay.h) == 3  # relabel, layout, scatter back
-        # a convergence rule keeps the in-kernel randomisation
+        # a convergence rule is decided on the device between the launches
         lay.layout_device(d, iters=1, batch=1024, max_batches=2, shuffle_seed=SEED, tol=1e-30)
         torch.cuda.synchronize()
-        assert bl.bl_driver_name(lay.h) == "two-barrier"
-        assert bl.bl_last_launch_count(lay.h) == 1
+        assert bl.bl_driver_name(lay.h) == "relabel+async"
         monkeypatch.setenv("BL_SHUFFLE_RELABEL", "0")
         lay.layout_device(d, iters=1, batch=1024, max_batches=2, shuffle_seed=SEED)
         torch.cuda.synchronize()
@@ -252,3 +251,28 @@ def test_relabelled_small_and_ragged_shapes(rows, cols, b):
     assert done == 1
     assert_positions_close(got, ref, POS_TOL, what=f"relabelled {rows}x{cols} b={b}")
     assert_energy_close(tr[:1], E[:1], tol=energy_gate(g, xy0, p), what=f"relabelled {rows}x{cols} b={b}")
+
+
+@pytest.mark.parametrize("mode", MODES, indirect=True)
+def test_shuffled_tol_stop_is_decided_on_the_device(mode):
+    """|E_t - E_{t-1}| < tol with randomised batches: the run stops
+    at the iteration a stop rule applied to its own free-running trace gives,
+    with that trace's prefix and that iteration's positions -- relabelled
+    iterations decide between their launches on the device (the later
+    launches of the call become no-ops), the in-kernel path inside its loop."""
+    g, xy0, cfg = build_config("C3b256")
+    p = _params(cfg, iters=12)
+    _, full, done = gpu_layout(g, xy0, **p)
+    assert done == 12
+    diffs = np.abs(np.diff(full))
+    # a tol that the trace crosses strictly inside the run
+    t_stop = 6
+    tol = float(np.sqrt(diffs[t_stop - 1] * diffs[t_stop - 2])) if diffs[t_stop - 1] < diffs[t_stop - 2] \
+        else float(diffs[t_stop - 1] * 1.000001)
+    stop = next(t for t in range(1, 12) if abs(full[t] - full[t - 1]) < tol) + 1
+    assert 2 <= stop < 12
+    ref_xy, _, _ = gpu_layout(g, xy0, **_params(cfg, iters=stop))
+    xy, tr, done = gpu_layout(g, xy0, **_params(cfg, iters=12, tol=tol))
+    assert done == stop
+    assert np.array_equal(tr, full[:stop])
+    assert np.array_equal(xy, ref_xy)
