@@ -633,7 +633,7 @@ static bl_status launch(bl_ctx *h, float2 *d_xy, const bl_params *p, cudaStream_
   // than BL_LCOOP entries per 8 batches; measured same box: C4 1,157 -> 1,295
   // it/s, relabelled C4 1.29 -> 0.94 ms per iteration; the hub-free configs
   // keep the plain instance, which the walk would cost 6 %)
-  k.lcoop = env_int("BL_LCOOP", (long long)h->n_long_rows * 8 >= k.nb ? 1 : 0);
+  k.lcoop = vt->T <= 2 ? env_int("BL_LCOOP", (long long)h->n_long_rows * 8 >= k.nb ? 1 : 0) : 0;
   const size_t smem = bl_smem_bytes(k.chunk4, k.red_cap);
   snprintf(h->kname_last, sizeof h->kname_last, "bl_layout_kernel<%d,%d,%d>", vt->NT, vt->T, vt->TP);
   h->driver_last = forces_mode ? "two-barrier"

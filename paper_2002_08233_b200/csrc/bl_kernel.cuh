@@ -2391,8 +2391,15 @@ __global__ void __launch_bounds__(NT, 1) bl_layout_kernel(BLKParams p) {
   if (p.pipelined == 3) {
     // two instances: the cooperative long-row walk costs the hub-free configs
     // 6 % when merely compiled into their loop (measured at C2 / C3)
-    if (p.lcoop) bl_run_lat<T, TP, true>(p, src4, tgt, red, sh);
-    else bl_run_lat<T, TP, false>(p, src4, tgt, red, sh);
+    // (only in the small-tile variants, which the latency driver runs by
+    // default: the host never sets lcoop for the others)
+    if constexpr (T <= 2) {
+      if (p.lcoop) {
+        bl_run_lat<T, TP, true>(p, src4, tgt, red, sh);
+        return;
+      }
+    }
+    bl_run_lat<T, TP, false>(p, src4, tgt, red, sh);
     return;
   }
   if (p.pipelined) {
